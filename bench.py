@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark: space-angle DOF-updates/s per sawtooth cycle (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl reference]
+
+Workload (default ``c4``): BASELINE config 4 — 1 group, cubic ConvFEM PG,
+512 x 512 cells, 2048 ordinates (angle grid 32 x 32 -> n_a = 16), seeded 32 x 32
+block materials, the largest configuration that fits one B200 and the one the
+metric's 1/2/4/8-GPU scaling is quoted on.  A step is one sawtooth cycle
+(flux/source assembly + the full multigrid cycle) of that solve, continuing the
+solve's own trajectory from psi = 0 (warm-up cycles first).  The per-cycle fields
+(2.3 GB each) exceed the 126 MB L2, so no flush is needed between steps.
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the CPU oracle port of
+the reference (oracle/, NumPy fp64, the reference is pure Python) on a bounded
+sample of the same workload.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+HBM_FALLBACK_GBS = 6650.0
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured", d
+    return HBM_FALLBACK_GBS, "fallback", {}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, n in enumerate(names):
+                if r[4 + k].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- workload
+def workload(name, nx=None):
+    from paper_2301_09991_b200 import benchmarks as B
+    if name == "c1":
+        return B.c1()
+    if name == "c2":
+        return B.c2()
+    if name == "c3":
+        return B.c3()
+    if name == "c4":
+        return B.c4() if nx is None else B.c4(nx=nx, blocks=nx // 16)
+    if name == "c5w":
+        return B.c5_weak(1)
+    raise SystemExit(f"unknown config {name}")
+
+
+def options_for(P, pd, dtype, cycles=None):
+    o = dict(pd.options)
+    pg = o.pop("pg", None)
+    if cycles is not None:
+        o["mg_iters"] = cycles
+    return P.SolverOptions(**o, pg=P.PGConfig(**(pg or {})), dtype=dtype)
+
+
+def bytes_model(pd, hier, live):
+    """Algorithmic fp32 bytes per cycle."""
+    n0 = pd.dof()
+    coarse = sum(l.grid.nx * l.grid.ny * l.quad.n_dir * pd.n_groups for l in hier.levels[1:])
+    if pd.options["scheme"] == "upwind" or pd.options.get("pg", {}).get("alpha_r", 3.0) == 0.0:
+        return 28 * n0 + 16 * coarse
+    return (64 if live else 56) * n0 + 16 * coarse
+
+
+# ----------------------------------------------------------------------------- reference arm
+def cpu_sample_problem(name):
+    """Bounded CPU sample of the workload for the oracle (fp64 NumPy, 1 core)."""
+    from paper_2301_09991_b200 import benchmarks as B
+    if name == "c4":
+        return B.c4(nx=64, blocks=4, n_a=8, cycles=1), "c4 generator at 64x64 cells, n_a=8 (512 ordinates), cubic PG"
+    if name == "c2":
+        return B.c2(nx=64, blocks=8, n_a=8, cycles=1), "c2 generator at 64x64 cells, n_a=8, quadratic PG"
+    if name == "c1":
+        return B.c1(cycles=1), "c1 full size"
+    if name == "c3":
+        return B.c3(n_pins=4, cells_per_pin=16, n_a=8, outers=1, inner=1), "c3 generator 64x64 cells, n_a=8, 2 groups"
+    return B.c4(nx=64, blocks=4, n_a=8, cycles=1), "c4 generator at 64x64 cells, n_a=8"
+
+
+def time_oracle_cycles(pd, steps, warmup):
+    """Run warmup + steps sawtooth cycles of the oracle; return per-cycle wall times."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import oracle as O
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _util import oracle_options, oracle_problem
+    st = O.setup(oracle_problem(pd), oracle_options(pd))
+    ng = pd.n_groups
+    data = O.padded(pd.nx, pd.ny, st.h, st.quad.n_dir, ng)
+    pgs = O.PGState(st.o.k_avg_theta)
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        phi = O.scalar_flux(data, st.h, st.quad.weights)
+        q = O.group_source(phi, st.mat)
+        O.sawtooth_cycle(data, q, st.levels, st.taps, st.o.order, st.o.pg, st.o.scheme,
+                         st.o.jacobi_sweeps, st.o.pg_sweeps, pgs)
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+    return times
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    pd, desc = cpu_sample_problem(args.config)
+    steps, warmup = args.steps, args.warmup
+    times = time_oracle_cycles(pd, steps, warmup)
+    dof = pd.dof()
+    total = float(sum(times))
+    value = dof * len(times) / total
+    line = {
+        "impl": "reference", "metric": "space-angle DOF-updates/s per sawtooth cycle",
+        "value": value, "unit": "DOF-updates/s", "n_gpus": args.gpus, "steps": steps,
+        "warmup": warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+        "config": {"workload": f"{args.config} (CPU sample: {desc})", "dof_per_step": dof},
+        "cpu_baseline": {"value": value, "unit": "DOF-updates/s", "cores": 1, "kind": "port",
+                         "sample": desc + f"; {steps} cycles after {warmup} warm-up; "
+                                          f"{cpu_model()}, 1 of {os.cpu_count()} cores"},
+        "e2e": {"value": value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- B200 arm
+def run_b200(args, rank, world, local_rank):
+    import torch
+    import paper_2301_09991_b200 as P
+    from paper_2301_09991_b200 import _lib
+    from paper_2301_09991_b200.problems import problem_from_data
+    from paper_2301_09991_b200.eigen import _buffers
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    lib = _lib.load()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    pd = workload(args.config, args.nx)
+    cycles_total = args.warmup + args.steps
+    opts = options_for(P, pd, args.dtype, cycles_total)
+    prob = problem_from_data(pd)
+    setup = P.setup_transport(prob, opts)
+    g = setup.grid
+    ng = pd.n_groups
+    dtype = opts.torch_dtype()
+    psi = P.Field(g, setup.quad.n_dir, ng, dtype=dtype, device=dev)
+    eng = setup.hierarchy.engine(ng, dtype, dev)
+    bufs = _buffers(setup, dtype, dev)
+    pgs = P.PGState(opts.k_avg_theta) if opts.scheme == "pg" else None
+    fission = None
+    # per-cycle source assembly exactly as _run_cycles does it
+    from paper_2301_09991_b200.eigen import assemble_group_source
+    from paper_2301_09991_b200.grid import scalar_flux_into
+    one_group = ng == 1
+
+    def one_cycle():
+        if not one_group:
+            scalar_flux_into(psi, setup.quad, bufs.phi)
+            assemble_group_source(bufs.phi, setup.mat, 0.0, dtype, bufs.q, fission)
+        return eng.cycle(psi, bufs.q, setup.filters, opts.pg, opts.scheme, opts.jacobi_sweeps,
+                         opts.pg_sweeps, pgs)
+
+    if one_group:
+        bufs.phi.zero_()
+        assemble_group_source(bufs.phi, setup.mat, 0.0, dtype, bufs.q, fission)
+    hist = []
+    frozen_before = []
+    for _ in range(args.warmup):
+        hist.append(one_cycle())
+    # ---- timed region: K cycles, device-timed with events, clocks sampled
+    eng.probe = {}
+    sampler = ClockSampler(local_rank)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    sampler.start()
+    n_launch0 = lib.csn_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        frozen_before.append(bool(pgs.frozen) if pgs is not None else False)
+        hist.append(one_cycle())
+    ev1.record()
+    torch.cuda.synchronize()
+    n_launch = lib.csn_launch_count() - n_launch0
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    probe = {k: [a.elapsed_time(b) for a, b in v] for k, v in eng.probe.items()}
+    eng.probe = None
+    dof = pd.dof()
+    value = dof * args.steps * world / (ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (fused PG sweep, K5): 20 B/DOF fp32
+    peak, peak_kind, peaks = measured_peaks()
+    esz = 4 if dtype == torch.float32 else 8
+    kernel_stats = {}
+    for k, ts in probe.items():
+        kernel_stats[k] = {"ms_avg": float(np.mean(ts)), "launches": len(ts)}
+    dominant = "pg_sweep" if "pg_sweep" in probe else "correction"
+    per_dof = {"pg_sweep": 5 * esz, "pg_residual": 4 * esz, "pg_diffusivity": 5 * esz,
+               "ema": 3 * esz, "correction": None}
+    roof = None
+    if dominant in probe and per_dof.get(dominant):
+        ms_k = float(np.mean(probe[dominant]))
+        achieved = per_dof[dominant] * dof / (ms_k * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak,
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback 6.65 TB/s",
+                "traffic": None,
+                "bytes_per_launch": per_dof[dominant] * dof, "ms_per_launch": ms_k,
+                "share_of_step": ms_k * len(probe[dominant]) / ms}
+    live = sum(1 for f in frozen_before if not f)
+    b_cycle = (bytes_model(pd, setup.hierarchy, True) * live
+               + bytes_model(pd, setup.hierarchy, False) * (args.steps - live)) / args.steps
+    cycle_roof = b_cycle / (ms / args.steps * 1e-3) / 1e9
+
+    # ---- end to end through the public API with host buffers (rank-local)
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = P.solve_fixed_source(prob, opts) if pd.driver == "fixed_source" else \
+            P.power_iteration(prob, opts, inner_iters=pd.inner_iters)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        ncyc = len(res.residual_history)
+        mf = setup.mat
+        h2d = sum(a.nbytes for a in (mf.sigma_s, mf.source, mf.nu_sigma_f, mf.chi))
+        h2d += sum(l.sigma_t.size * esz for l in setup.hierarchy.levels)
+        d2h = res.phi.nbytes + 8 * ncyc
+        e2e = {"value": dof * ncyc * world / wall, "unit": "DOF-updates/s",
+               "h2d_bytes_per_step": h2d / ncyc, "d2h_bytes_per_step": d2h / ncyc,
+               "cycles": ncyc, "wall_s": wall,
+               "note": "solve_fixed_source/power_iteration call incl. setup, uploads, phi read-back"}
+
+    # ---- CPU baseline (oracle port, bounded sample, rank 0 at N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        spd, desc = cpu_sample_problem(args.config)
+        ts = time_oracle_cycles(spd, 1, 0)
+        cpu = {"value": spd.dof() / ts[0], "unit": "DOF-updates/s", "cores": 1, "kind": "port",
+               "sample": f"{desc}; 1 cycle; {cpu_model()}, 1 of {os.cpu_count()} cores"}
+
+    if rank == 0:
+        line = {
+            "metric": "space-angle DOF-updates/s per sawtooth cycle",
+            "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if dtype == torch.float32 else "f64",
+            "data": "synthetic (seeded BASELINE generators, paper_2301_09991_b200/benchmarks.py)",
+            "config": {"workload": f"{args.config}: " + {
+                "c4": "1 group, cubic PG, 512x512 cells, 2048 ordinates (n_a=16), 32x32 seeded blocks",
+                "c2": "1 group, quadratic PG, 128x128 cells, 512 ordinates, 8x8 seeded blocks",
+                "c1": "1 group, linear, PG off (alpha_r=0), 64x64, 128 ordinates",
+                "c3": "2-group eigen, linear PG, 256x256, 512 ordinates",
+                "c5w": "7-group eigen, linear PG, 512x512 per GPU, 2048 ordinates"}.get(args.config, ""),
+                "dof_per_cycle": dof, "nx": pd.nx, "ny": pd.ny, "ordinates": 8 * pd.n_a ** 2,
+                "groups": ng, "order": pd.options["order"], "levels": setup.hierarchy.n_levels,
+                "live_cycles": live, "frozen_cycles": args.steps - live,
+                "l2": "fields 2.3 GB >> 126 MB L2 (no flush needed)" if args.config == "c4" else "see DESIGN.md",
+                "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+            "roofline": roof,
+            "cycle_roofline": {"bytes_per_cycle": b_cycle, "achieved": cycle_roof, "peak": peak,
+                               "unit": "GB/s", "frac": cycle_roof / peak},
+            "kernels": kernel_stats,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(n_launch),
+            "clocks": clocks,
+            "residual_history": hist,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=17)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--nx", type=int, default=None, help="override the cell count (c4 only)")
+    ap.add_argument("--dtype", default="float32")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 0 or args.steps < 1:
+        raise SystemExit("need --steps >= 1")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    run_b200(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

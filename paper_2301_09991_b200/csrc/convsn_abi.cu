@@ -1,0 +1,493 @@
+// extern "C" entry points of libconvsn_sm100.so (declared in include/convsn_sm100.h).
+// Argument checking, launch geometry and float/double x ConvFEM-order dispatch.
+#include <math.h>
+#include <string.h>
+
+#include "common.cuh"
+#include "misc_kernels.cuh"
+#include "pg_kernels.cuh"
+#include "upwind_kernels.cuh"
+
+using namespace csn;
+
+unsigned long long csn::g_launches = 0;
+
+namespace {
+
+constexpr int kVersion = 1;
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline bool geom_ok(const csn_geom* g) {
+    return g && g->nx >= 1 && g->ny >= 1 && g->nd >= 1 && g->ng >= 1 && g->dx > 0 && g->dy > 0;
+}
+
+inline int grid1d(int64_t n, int block = 256) {
+    int64_t b = cdiv(n, block);
+    if (b > 148 * 64) b = 148 * 64;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+// rows per CTA chunk for the y-marching kernels: enough CTAs to fill 148 SMs ~4x
+inline int pick_ly(int64_t ctas_xy, int rows, int T) {
+    int chunks = 1;
+    while (ctas_xy * chunks < 148 * 4 && rows / (chunks * 2) >= 4 * T) chunks *= 2;
+    int ly = (int)cdiv(rows, chunks);
+    ly = (int)cdiv(ly, T) * T;
+    return ly;
+}
+
+template <class Real, int L>
+PGTaps<Real, L> make_taps(const double* taps, double dx, double dy) {
+    PGTaps<Real, L> t;
+    constexpr int T = 2 * L + 1;
+    const double* m = taps;
+    const double* gr = taps + T;
+    const double* st = taps + 2 * T;
+    for (int a = 0; a < T; ++a) {
+        t.m[a] = (Real)m[a];
+        t.gx[a] = (Real)(gr[a] / dx);
+        t.gy[a] = (Real)(gr[a] / dy);
+        t.sx[a] = (Real)(st[a] / (dx * dx));
+        t.sy[a] = (Real)(st[a] / (dy * dy));
+    }
+    return t;
+}
+
+// ------------------------------------------------------------------ PG residual
+template <class Real, int L>
+int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int psi_h,
+                     const void* delta, int delta_h, const void* kx, const void* ky, int k_h,
+                     const void* sigma, const void* q, int q_per_dof, const void* mu,
+                     const void* nu, const void* strm, void* r, int r_h, void* out, int out_h,
+                     double beta, double* partials, double* l1, cudaStream_t st) {
+    constexpr int T = 2 * L + 1;
+    if (k_h < L) return CSN_E_ARG;
+    PGResidArgs<Real, L> a;
+    a.g = make_geo(*g);
+    a.t = make_taps<Real, L>(taps, g->dx, g->dy);
+    a.psi = (const Real*)psi; a.psi_h = psi_h;
+    a.delta = (const Real*)delta; a.delta_h = delta_h;
+    a.kx = (const Real*)kx; a.ky = (const Real*)ky; a.k_h = k_h;
+    a.sigma = (const Real*)sigma; a.q = (const Real*)q; a.q_per_dof = q_per_dof;
+    a.mu = (const Real*)mu; a.nu = (const Real*)nu; a.strm = (const Real*)strm;
+    a.r = (Real*)r; a.r_h = r_h;
+    a.out = (Real*)out; a.out_h = out_h; a.beta = (Real)beta;
+    const int gx = (int)cdiv(g->nx, PG_TX);
+    const int gy = (int)cdiv((int64_t)g->nd * g->ng, PG_CC);
+    a.ly = pick_ly((int64_t)gx * gy, g->ny, T);
+    const int gz = (int)cdiv(g->ny, a.ly);
+    a.partials = (l1 || partials) ? partials : nullptr;
+    dim3 grid(gx, gy, gz), block(PG_CC, PG_TX);
+    if (out) {
+        pg_residual_kernel<Real, L, true><<<grid, block, 0, st>>>(a);
+        CSN_CHECK_LAUNCH();
+    } else {
+        if (l1 && !partials) return CSN_E_ARG;
+        pg_residual_kernel<Real, L, false><<<grid, block, 0, st>>>(a);
+        CSN_CHECK_LAUNCH();
+        if (l1) {
+            sum_f64_kernel<<<1, 1024, 0, st>>>(partials, (int64_t)gx * gy * gz, 1.0, l1);
+            CSN_CHECK_LAUNCH();
+        }
+    }
+    return CSN_OK;
+}
+
+template <class Real, int L>
+int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const void* psi,
+              int psi_h, const void* avg_in, int avg_in_h, void* avg_out, int avg_out_h,
+              int avg_mode, double theta, const void* mu, const void* nu, void* kx, void* ky,
+              int k_h, cudaStream_t st) {
+    constexpr int T = 2 * L + 1;
+    constexpr int TXO = K_TXS - 2 * L;
+    if (k_h < L) return CSN_E_ARG;
+    if (avg_mode < 0 || avg_mode > 2) return CSN_E_SCHEME;
+    if (avg_mode >= 1 && !avg_out) return CSN_E_ARG;
+    if (avg_mode == 2 && (!avg_in || avg_in == avg_out)) return CSN_E_ARG;
+    PGKArgs<Real, L> a;
+    a.g = make_geo(*g);
+    a.t = make_taps<Real, L>(taps, g->dx, g->dy);
+    a.psi = (const Real*)psi; a.psi_h = psi_h;
+    a.avg_in = (const Real*)avg_in; a.avg_in_h = avg_in_h;
+    a.avg_out = (Real*)avg_out; a.avg_out_h = avg_out_h;
+    a.avg_mode = avg_mode; a.theta = (Real)theta; a.omt = (Real)(1.0 - theta);
+    a.eps = (Real)cfg[0]; a.alpha_r = (Real)cfg[1]; a.a_abs = (Real)cfg[2]; a.a_sq = (Real)cfg[3];
+    a.dx = (Real)g->dx; a.dy = (Real)g->dy;
+    a.mu = (const Real*)mu; a.nu = (const Real*)nu;
+    a.kx = (Real*)kx; a.ky = (Real*)ky; a.k_h = k_h;
+    const int gx = (int)cdiv(g->nx + 2 * L, TXO);
+    const int gy = (int)cdiv((int64_t)g->nd * g->ng, PG_CC);
+    a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T);
+    const int gz = (int)cdiv(g->ny + 2 * L, a.ly);
+    dim3 grid(gx, gy, gz), block(PG_CC, K_TXS);
+    pg_diffusivity_kernel<Real, L><<<grid, block, 0, st>>>(a);
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
+template <class Real>
+int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int init_mode,
+                       const void* init, int init_h, const csn_geom* gc, const void* sigma,
+                       const void* mu, const void* nu, const void* strm, int n_sweeps,
+                       double diag_scale, void* out, int out_h, cudaStream_t st) {
+    constexpr int CC = sizeof(Real) == 4 ? 16 : 8;
+    UpSmoothArgs<Real> a;
+    a.g = make_geo(*g);
+    a.src = (const Real*)src; a.q_per_dof = q_per_dof;
+    a.init_mode = init_mode; a.init = (const Real*)init; a.init_h = init_h;
+    a.angle_coarsens = 0;
+    if (init_mode == 2) {
+        a.gc = make_geo(*gc);
+        if (gc->nx * 2 != g->nx || gc->ny * 2 != g->ny || gc->ng != g->ng) return CSN_E_ARG;
+        if (gc->na == g->na) a.angle_coarsens = 0;
+        else if (gc->na * 2 == g->na) a.angle_coarsens = 1;
+        else return CSN_E_ARG;
+    } else {
+        a.gc = a.g;
+    }
+    a.sigma = (const Real*)sigma; a.mu = (const Real*)mu; a.nu = (const Real*)nu;
+    a.strm = (const Real*)strm;
+    a.dx = (Real)g->dx; a.dy = (Real)g->dy;
+    a.scale = (Real)diag_scale; a.use_scale = diag_scale != 1.0;
+    a.out = (Real*)out; a.out_h = out_h;
+    const int tiles = (int)(cdiv(g->nx, UP_T) * cdiv(g->ny, UP_T));
+    const int gy = (int)cdiv((int64_t)g->nd * g->ng, CC);
+    const size_t smem = (size_t)3 * UP_W * UP_W * CC * sizeof(Real);
+    static_assert((size_t)3 * UP_W * UP_W * CC * sizeof(Real) <= 48 * 1024, "smem");
+    a.n_sweeps = n_sweeps;
+    upwind_smooth_kernel<Real, CC><<<dim3(tiles, gy), 256, smem, st>>>(a);
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
+#define DTYPE_DISPATCH(dtype, FN, ...)                         \
+    ((dtype) == CSN_F32 ? FN<float>(__VA_ARGS__)               \
+     : (dtype) == CSN_F64 ? FN<double>(__VA_ARGS__) : CSN_E_DTYPE)
+
+}  // namespace
+
+extern "C" {
+
+int csn_version(void) { return kVersion; }
+
+unsigned long long csn_launch_count(void) { return g_launches; }
+
+const char* csn_error_string(int code) {
+    switch (code) {
+        case CSN_OK: return "ok";
+        case CSN_E_ARG: return "invalid argument";
+        case CSN_E_ORDER: return "unsupported ConvFEM order (expected 1, 2, 3 or 5)";
+        case CSN_E_DTYPE: return "unsupported dtype";
+        case CSN_E_SCHEME: return "unsupported mode";
+        default: break;
+    }
+    if (code < 0) return cudaGetErrorString((cudaError_t)(-code));
+    return "unknown error";
+}
+
+int64_t csn_partials_size(int dtype, const csn_geom* g, int order) {
+    (void)dtype;
+    if (!geom_ok(g)) return -CSN_E_ARG;
+    const int64_t C = (int64_t)g->nd * g->ng;
+    int64_t pg = cdiv(g->nx, PG_TX) * cdiv(C, PG_CC) * (int64_t)g->ny;   // upper bound (ly >= 1)
+    int64_t up = grid1d((int64_t)g->nx * g->ny * C);
+    int64_t cells = grid1d((int64_t)g->nx * g->ny * g->ng);
+    (void)order;
+    int64_t m = pg > up ? pg : up;
+    return m > cells ? m : cells;
+}
+
+int csn_apply_boundary(int dtype, const csn_geom* g, void* f, int halo, const void* mu,
+                       const void* nu, void* stream) {
+    if (!geom_ok(g) || !f || !mu || !nu || halo < 0) return CSN_E_ARG;
+    if (halo == 0) return CSN_OK;
+    Geo d = make_geo(*g);
+    const int64_t total = ((int64_t)2 * halo * (g->ny + 2 * halo) + (int64_t)g->nx * 2 * halo) * d.C;
+    if (dtype == CSN_F32)
+        boundary_kernel<float><<<grid1d(total), 256, 0, S(stream)>>>(d, (float*)f, halo,
+                                                                      (const float*)mu, (const float*)nu);
+    else if (dtype == CSN_F64)
+        boundary_kernel<double><<<grid1d(total), 256, 0, S(stream)>>>(d, (double*)f, halo,
+                                                                       (const double*)mu, (const double*)nu);
+    else return CSN_E_DTYPE;
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
+int csn_upwind_residual(int dtype, const csn_geom* g, const void* psi, int psi_halo,
+                        const void* sigma, const void* q, int q_per_dof, const void* mu,
+                        const void* nu, void* r, int r_halo, double* partials, double* l1,
+                        void* stream) {
+    if (!geom_ok(g) || !psi || !sigma || !q || !mu || !nu || psi_halo < 1) return CSN_E_ARG;
+    if (l1 && !partials) return CSN_E_ARG;
+    const int64_t total = (int64_t)g->nx * g->ny * g->nd * g->ng;
+    const int nb = grid1d(total);
+    auto run = [&](auto tag) -> int {
+        using Real = decltype(tag);
+        UpResArgs<Real> a;
+        a.g = make_geo(*g);
+        a.psi = (const Real*)psi; a.psi_h = psi_halo;
+        a.sigma = (const Real*)sigma; a.q = (const Real*)q; a.q_per_dof = q_per_dof;
+        a.mu = (const Real*)mu; a.nu = (const Real*)nu;
+        a.dx = (Real)g->dx; a.dy = (Real)g->dy;
+        a.r = (Real*)r; a.r_h = r_halo;
+        a.partials = l1 ? partials : nullptr;
+        upwind_residual_kernel<Real><<<nb, 256, 0, S(stream)>>>(a);
+        CSN_CHECK_LAUNCH();
+        if (l1) {
+            sum_f64_kernel<<<1, 1024, 0, S(stream)>>>(partials, nb, 1.0, l1);
+            CSN_CHECK_LAUNCH();
+        }
+        return CSN_OK;
+    };
+    if (dtype == CSN_F32) return run(float());
+    if (dtype == CSN_F64) return run(double());
+    return CSN_E_DTYPE;
+}
+
+int csn_upwind_smooth(int dtype, const csn_geom* g, const void* src, int q_per_dof,
+                      int init_mode, const void* init, int init_halo, const csn_geom* gc,
+                      const void* sigma, const void* mu, const void* nu, const void* strm,
+                      int n_sweeps, double diag_scale, void* out, int out_halo, void* stream) {
+    if (!geom_ok(g) || !src || !sigma || !mu || !nu || !strm || !out || n_sweeps < 0 ||
+        n_sweeps > UP_H)
+        return CSN_E_ARG;
+    if (init_mode < 0 || init_mode > 2) return CSN_E_SCHEME;
+    if (init_mode > 0 && !init) return CSN_E_ARG;
+    if (init_mode == 2 && !geom_ok(gc)) return CSN_E_ARG;
+    if (init_mode == 1 && init == out && n_sweeps > 0) return CSN_E_ARG;
+    return DTYPE_DISPATCH(dtype, upwind_smooth_impl, g, src, q_per_dof, init_mode, init, init_halo,
+                          gc, sigma, mu, nu, strm, n_sweeps, diag_scale, out, out_halo, S(stream));
+}
+
+int csn_restrict(int dtype, const csn_geom* gf, const csn_geom* gc, const void* fine,
+                 int fine_halo, const void* w_f, const void* w_c, int normalise, void* coarse,
+                 int coarse_halo, void* stream) {
+    if (!geom_ok(gf) || !geom_ok(gc) || !fine || !w_f || !coarse) return CSN_E_ARG;
+    if (normalise && !w_c) return CSN_E_ARG;
+    if (gc->nx * 2 != gf->nx || gc->ny * 2 != gf->ny || gc->ng != gf->ng) return CSN_E_ARG;
+    int ac;
+    if (gc->na == gf->na) ac = 0;
+    else if (gc->na * 2 == gf->na) ac = 1;
+    else return CSN_E_ARG;
+    const int64_t total = (int64_t)gc->nx * gc->ny * gc->nd * gc->ng;
+    auto run = [&](auto tag) -> int {
+        using Real = decltype(tag);
+        RestrictArgs<Real> a;
+        a.gf = make_geo(*gf); a.gc = make_geo(*gc);
+        a.fine = (const Real*)fine; a.fine_h = fine_halo;
+        a.wf = (const Real*)w_f; a.wc = (const Real*)w_c;
+        a.af = (Real)(gf->dx * gf->dy); a.ac = (Real)(gc->dx * gc->dy);
+        a.angle_coarsens = ac; a.normalise = normalise;
+        a.coarse = (Real*)coarse; a.coarse_h = coarse_halo;
+        restrict_kernel<Real><<<grid1d(total), 256, 0, S(stream)>>>(a);
+        CSN_CHECK_LAUNCH();
+        return CSN_OK;
+    };
+    if (dtype == CSN_F32) return run(float());
+    if (dtype == CSN_F64) return run(double());
+    return CSN_E_DTYPE;
+}
+
+int csn_prolong(int dtype, const csn_geom* gc, const csn_geom* gf, const void* coarse,
+                int coarse_halo, void* fine, int fine_halo, void* stream) {
+    if (!geom_ok(gf) || !geom_ok(gc) || !fine || !coarse) return CSN_E_ARG;
+    if (gc->nx * 2 != gf->nx || gc->ny * 2 != gf->ny || gc->ng != gf->ng) return CSN_E_ARG;
+    int ac;
+    if (gc->na == gf->na) ac = 0;
+    else if (gc->na * 2 == gf->na) ac = 1;
+    else return CSN_E_ARG;
+    const int64_t total = (int64_t)gf->nx * gf->ny * gf->nd * gf->ng;
+    auto run = [&](auto tag) -> int {
+        using Real = decltype(tag);
+        ProlongArgs<Real> a;
+        a.gc = make_geo(*gc); a.gf = make_geo(*gf);
+        a.coarse = (const Real*)coarse; a.coarse_h = coarse_halo;
+        a.angle_coarsens = ac;
+        a.fine = (Real*)fine; a.fine_h = fine_halo;
+        prolong_kernel<Real><<<grid1d(total), 256, 0, S(stream)>>>(a);
+        CSN_CHECK_LAUNCH();
+        return CSN_OK;
+    };
+    if (dtype == CSN_F32) return run(float());
+    if (dtype == CSN_F64) return run(double());
+    return CSN_E_DTYPE;
+}
+
+#define ORDER_DISPATCH(FN, ...)                                                         \
+    switch (order) {                                                                    \
+        case 1: return dtype == CSN_F32 ? FN<float, 1>(__VA_ARGS__) : FN<double, 1>(__VA_ARGS__); \
+        case 2: return dtype == CSN_F32 ? FN<float, 2>(__VA_ARGS__) : FN<double, 2>(__VA_ARGS__); \
+        case 3: return dtype == CSN_F32 ? FN<float, 3>(__VA_ARGS__) : FN<double, 3>(__VA_ARGS__); \
+        case 5: return dtype == CSN_F32 ? FN<float, 5>(__VA_ARGS__) : FN<double, 5>(__VA_ARGS__); \
+        default: return CSN_E_ORDER;                                                    \
+    }
+
+int csn_pg_diffusivities(int dtype, int order, const csn_geom* g, const double* taps,
+                         const double* cfg, const void* psi, int psi_halo, const void* avg_in,
+                         int avg_in_halo, void* avg_out, int avg_out_halo, int avg_mode,
+                         double theta, const void* mu, const void* nu, void* kx, void* ky,
+                         int k_halo, void* stream) {
+    if (!geom_ok(g) || !taps || !cfg || !psi || !mu || !nu || !kx || !ky) return CSN_E_ARG;
+    if (dtype != CSN_F32 && dtype != CSN_F64) return CSN_E_DTYPE;
+    ORDER_DISPATCH(pg_k_impl, g, taps, cfg, psi, psi_halo, avg_in, avg_in_halo, avg_out,
+                   avg_out_halo, avg_mode, theta, mu, nu, kx, ky, k_halo, S(stream));
+}
+
+int csn_pg_residual(int dtype, int order, const csn_geom* g, const double* taps,
+                    const void* psi, int psi_halo, const void* delta, int delta_halo,
+                    const void* kx, const void* ky, int k_halo, const void* sigma, const void* q,
+                    int q_per_dof, const void* mu, const void* nu, const void* strm, void* r,
+                    int r_halo, void* psi_out, int psi_out_halo, double beta, double* partials,
+                    double* l1, void* stream) {
+    if (!geom_ok(g) || !taps || !psi || !kx || !ky || !sigma || !q || !mu || !nu)
+        return CSN_E_ARG;
+    if (psi_out && (!strm || psi_out == psi)) return CSN_E_ARG;
+    if (dtype != CSN_F32 && dtype != CSN_F64) return CSN_E_DTYPE;
+    ORDER_DISPATCH(pg_residual_impl, g, taps, psi, psi_halo, delta, delta_halo, kx, ky, k_halo,
+                   sigma, q, q_per_dof, mu, nu, strm, r, r_halo, psi_out, psi_out_halo, beta,
+                   partials, l1, S(stream));
+}
+
+int csn_scalar_flux(int dtype, const csn_geom* g, const void* psi, int halo, const void* w,
+                    double* phi, void* stream) {
+    if (!geom_ok(g) || !psi || !w || !phi || halo < 0) return CSN_E_ARG;
+    Geo d = make_geo(*g);
+    const int64_t warps = (int64_t)g->nx * g->ny * g->ng;
+    const int nb = grid1d(warps * 32);
+    if (dtype == CSN_F32)
+        scalar_flux_kernel<float><<<nb, 256, 0, S(stream)>>>(d, (const float*)psi, halo, (const float*)w, phi);
+    else if (dtype == CSN_F64)
+        scalar_flux_kernel<double><<<nb, 256, 0, S(stream)>>>(d, (const double*)psi, halo, (const double*)w, phi);
+    else return CSN_E_DTYPE;
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
+int csn_group_source(int dtype, const csn_geom* g, const double* phi, const double* sigma_s,
+                     const double* source, const double* fission, double lam, const double* chi,
+                     const double* nsf, void* q, void* stream) {
+    if (!geom_ok(g) || !phi || !sigma_s || !source || !q) return CSN_E_ARG;
+    if (lam != 0.0 && (!chi || !nsf)) return CSN_E_ARG;
+    Geo d = make_geo(*g);
+    const int nb = grid1d((int64_t)g->nx * g->ny * g->ng);
+    if (dtype == CSN_F32)
+        group_source_kernel<float><<<nb, 256, 0, S(stream)>>>(d, phi, sigma_s, source, fission, lam, chi, nsf, (float*)q);
+    else if (dtype == CSN_F64)
+        group_source_kernel<double><<<nb, 256, 0, S(stream)>>>(d, phi, sigma_s, source, fission, lam, chi, nsf, (double*)q);
+    else return CSN_E_DTYPE;
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
+int csn_fission_source(const csn_geom* g, const double* phi, const double* chi,
+                       const double* nsf, double inv_k, double* out, void* stream) {
+    if (!geom_ok(g) || !phi || !chi || !nsf || !out) return CSN_E_ARG;
+    Geo d = make_geo(*g);
+    fission_source_kernel<<<grid1d((int64_t)g->nx * g->ny * g->ng), 256, 0, S(stream)>>>(d, phi, chi, nsf, inv_k, out);
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
+int csn_production(const csn_geom* g, const double* phi, const double* nsf, double* partials,
+                   double* out, void* stream) {
+    if (!geom_ok(g) || !phi || !nsf || !partials || !out) return CSN_E_ARG;
+    const int64_t n = (int64_t)g->nx * g->ny * g->ng;
+    const int nb = grid1d(n);
+    dot_partials_kernel<<<nb, 256, 0, S(stream)>>>(nsf, phi, n, partials);
+    CSN_CHECK_LAUNCH();
+    sum_f64_kernel<<<1, 1024, 0, S(stream)>>>(partials, nb, g->dx * g->dy, out);
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
+int csn_sum_f64(const double* x, int64_t n, double* out, void* stream) {
+    if (!x || !out || n < 0) return CSN_E_ARG;
+    sum_f64_kernel<<<1, 1024, 0, S(stream)>>>(x, n, 1.0, out);
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
+int csn_scale(int dtype, void* x, int64_t n, double s, int divide, void* stream) {
+    if (!x || n < 0) return CSN_E_ARG;
+    if (n == 0) return CSN_OK;
+    if (dtype == CSN_F32)
+        scale_kernel<float><<<grid1d(n), 256, 0, S(stream)>>>((float*)x, n, (float)s, divide);
+    else if (dtype == CSN_F64)
+        scale_kernel<double><<<grid1d(n), 256, 0, S(stream)>>>((double*)x, n, s, divide);
+    else return CSN_E_DTYPE;
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
+int csn_sub_interior(int dtype, const csn_geom* g, void* psi, int psi_halo, const void* delta,
+                     int delta_halo, void* stream) {
+    if (!geom_ok(g) || !psi || !delta) return CSN_E_ARG;
+    Geo d = make_geo(*g);
+    const int nb = grid1d((int64_t)g->nx * g->ny * d.C);
+    if (dtype == CSN_F32)
+        sub_interior_kernel<float><<<nb, 256, 0, S(stream)>>>(d, (float*)psi, psi_halo, (const float*)delta, delta_halo);
+    else if (dtype == CSN_F64)
+        sub_interior_kernel<double><<<nb, 256, 0, S(stream)>>>(d, (double*)psi, psi_halo, (const double*)delta, delta_halo);
+    else return CSN_E_DTYPE;
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
+int csn_ema(int dtype, const csn_geom* g, void* avg, int avg_halo, const void* psi,
+            int psi_halo, double theta, int mode, void* stream) {
+    if (!geom_ok(g) || !avg || !psi) return CSN_E_ARG;
+    if (mode != 1 && mode != 2) return CSN_E_SCHEME;
+    Geo d = make_geo(*g);
+    const int nb = grid1d((int64_t)g->nx * g->ny * d.C);
+    if (dtype == CSN_F32)
+        ema_kernel<float><<<nb, 256, 0, S(stream)>>>(d, (float*)avg, avg_halo, (const float*)psi, psi_halo, (float)theta, (float)(1.0 - theta), mode);
+    else if (dtype == CSN_F64)
+        ema_kernel<double><<<nb, 256, 0, S(stream)>>>(d, (double*)avg, avg_halo, (const double*)psi, psi_halo, theta, 1.0 - theta, mode);
+    else return CSN_E_DTYPE;
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
+int csn_convolve(int dtype, const csn_geom* g, const void* src, int halo, const double* stencil,
+                 int width, int margin, const void* dir_scale, void* out, void* stream) {
+    if (!geom_ok(g) || !src || !stencil || !out || width < 1 || width > 11 || !(width & 1))
+        return CSN_E_ARG;
+    if (margin < 0 || margin + (width - 1) / 2 > halo) return CSN_E_ARG;
+    Geo d = make_geo(*g);
+    StencilW w;
+    memset(&w, 0, sizeof(w));
+    memcpy(w.w, stencil, sizeof(double) * width * width);
+    const int64_t total = (int64_t)(g->nx + 2 * halo) * (g->ny + 2 * halo) * d.C;
+    if (dtype == CSN_F32)
+        convolve_kernel<float><<<grid1d(total), 256, 0, S(stream)>>>(d, (const float*)src, halo, w, width, margin, (const float*)dir_scale, (float*)out);
+    else if (dtype == CSN_F64)
+        convolve_kernel<double><<<grid1d(total), 256, 0, S(stream)>>>(d, (const double*)src, halo, w, width, margin, (const double*)dir_scale, (double*)out);
+    else return CSN_E_DTYPE;
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
+int csn_pass1d(int dtype, const csn_geom* g, const void* src, int halo, const double* taps,
+               int width, int axis, int margin, void* out, void* stream) {
+    if (!geom_ok(g) || !src || !taps || !out || width < 1 || width > 121 || !(width & 1))
+        return CSN_E_ARG;
+    if (axis != 0 && axis != 1) return CSN_E_ARG;
+    if (margin < 0 || margin + (width - 1) / 2 > halo) return CSN_E_ARG;
+    Geo d = make_geo(*g);
+    StencilW w;
+    memset(&w, 0, sizeof(w));
+    memcpy(w.w, taps, sizeof(double) * width);
+    const int64_t total = (int64_t)(g->nx + 2 * halo) * (g->ny + 2 * halo) * d.C;
+    if (dtype == CSN_F32)
+        pass1d_kernel<float><<<grid1d(total), 256, 0, S(stream)>>>(d, (const float*)src, halo, w, width, axis, margin, (float*)out);
+    else if (dtype == CSN_F64)
+        pass1d_kernel<double><<<grid1d(total), 256, 0, S(stream)>>>(d, (const double*)src, halo, w, width, axis, margin, (double*)out);
+    else return CSN_E_DTYPE;
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
+}  // extern "C"

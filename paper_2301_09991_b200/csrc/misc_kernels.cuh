@@ -1,0 +1,312 @@
+// Transfers (R/multigrid.py:110-146,342-353), boundary fill (R/grid.py:165-190),
+// scalar flux (R/grid.py:193-198), group source / fission (R/eigen.py:117-135),
+// generic stencils (R/grid.py:85-162) and small vector utilities.
+#pragma once
+#include "common.cuh"
+
+namespace csn {
+
+// ------------------------------------------------------------------ restriction
+// s_c[I,J,N] = sum_{2x2 cells} sum_{children n of N} r[i,j,n] w_n dxf dyf  (raw),
+// divided by w_N dxc dyc when normalise (R/multigrid.py:326).
+template <class Real>
+struct RestrictArgs {
+    Geo gf, gc;
+    const Real* fine; int fine_h;
+    const Real* wf; const Real* wc;
+    Real af, ac;      // cell areas
+    int angle_coarsens, normalise;
+    Real* coarse; int coarse_h;
+};
+
+template <class Real>
+__global__ void __launch_bounds__(256) restrict_kernel(const RestrictArgs<Real> a) {
+    const Geo &gf = a.gf, &gc = a.gc;
+    const int64_t total = (int64_t)gc.nx * gc.ny * gc.C;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int cc = (int)(e % gc.C);
+        const int64_t cell = e / gc.C;
+        const int J = (int)(cell % gc.ny), I = (int)(cell / gc.ny);
+        const int N = cc / gc.ng, g = cc - N * gc.ng;
+        Real acc = Real(0);
+        if (a.angle_coarsens) {
+            const int naf = gf.na, nac = gc.na;
+            const int f = N / (nac * nac), rem = N - f * nac * nac;
+            const int R = rem / nac, Cc = rem - R * nac;
+#pragma unroll
+            for (int pa = 0; pa < 2; ++pa)
+#pragma unroll
+                for (int pb = 0; pb < 2; ++pb) {
+                    const int nf = f * naf * naf + (2 * R + pa) * naf + (2 * Cc + pb);
+                    const int cf = nf * gf.ng + g;
+                    const Real wn = a.wf[nf];
+                    Real sp = Real(0);
+#pragma unroll
+                    for (int i = 0; i < 2; ++i)
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            sp += a.fine[fidx(2 * I + i, 2 * J + j, cf, gf.ny, a.fine_h, gf.C)] * wn * a.af;
+                    acc += sp;
+                }
+        } else {
+            const Real wn = a.wf[N];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                    acc += a.fine[fidx(2 * I + i, 2 * J + j, cc, gf.ny, a.fine_h, gf.C)] * wn * a.af;
+        }
+        if (a.normalise) acc /= a.wc[N] * a.ac;
+        a.coarse[fidx(I, J, cc, gc.ny, a.coarse_h, gc.C)] = acc;
+    }
+}
+
+template <class Real>
+struct ProlongArgs {
+    Geo gc, gf;
+    const Real* coarse; int coarse_h;
+    int angle_coarsens;
+    Real* fine; int fine_h;
+};
+
+template <class Real>
+__global__ void __launch_bounds__(256) prolong_kernel(const ProlongArgs<Real> a) {
+    const Geo &gf = a.gf, &gc = a.gc;
+    const int64_t total = (int64_t)gf.nx * gf.ny * gf.C;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e % gf.C);
+        const int64_t cell = e / gf.C;
+        const int y = (int)(cell % gf.ny), x = (int)(cell / gf.ny);
+        int pc = c;
+        if (a.angle_coarsens) {
+            const int n = c / gf.ng, g = c - n * gf.ng;
+            const int naf = gf.na, nac = gc.na, per = naf * naf;
+            const int f = n / per, rem = n - f * per;
+            const int row = rem / naf, col = rem - row * naf;
+            pc = (f * nac * nac + (row >> 1) * nac + (col >> 1)) * gf.ng + g;
+        }
+        a.fine[fidx(x, y, c, gf.ny, a.fine_h, gf.C)] =
+            a.coarse[fidx(x >> 1, y >> 1, pc, gc.ny, a.coarse_h, gc.C)];
+    }
+}
+
+// ------------------------------------------------------------------ boundary fill
+template <class Real>
+__global__ void __launch_bounds__(256)
+boundary_kernel(Geo g, Real* f, int h, const Real* mu, const Real* nu) {
+    // iterate over halo cells only: rows [0, h) and [nx+h, nx+2h) fully, plus the
+    // left/right h columns of the interior rows
+    const int NY = g.ny + 2 * h;
+    const int64_t n_rowcells = (int64_t)2 * h * NY;
+    const int64_t n_colcells = (int64_t)g.nx * 2 * h;
+    const int64_t total = (n_rowcells + n_colcells) * g.C;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e % g.C);
+        int64_t k = e / g.C;
+        int xs, ys;   // storage coordinates
+        if (k < n_rowcells) {
+            const int r = (int)(k / NY);
+            ys = (int)(k % NY);
+            xs = r < h ? r : g.nx + r;
+        } else {
+            k -= n_rowcells;
+            const int r = (int)(k / (2 * h));
+            const int cidx = (int)(k % (2 * h));
+            xs = h + r;
+            ys = cidx < h ? cidx : g.ny + cidx;
+        }
+        const int n = c / g.ng;
+        const bool mpos = mu[n] > Real(0), npos = nu[n] > Real(0);
+        int x = xs - h, y = ys - h;
+        Real v = Real(0);
+        if (resolve_vac(x, y, g, mpos, npos)) v = f[fidx(x, y, c, g.ny, h, g.C)];
+        f[((int64_t)xs * NY + ys) * g.C + c] = v;
+    }
+}
+
+// ------------------------------------------------------------------ scalar flux
+// one warp per (cell, group); fp64 accumulation, fixed shuffle tree.
+template <class Real>
+__global__ void __launch_bounds__(256)
+scalar_flux_kernel(Geo g, const Real* psi, int h, const Real* w, double* phi) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t total = (int64_t)g.nx * g.ny * g.ng;
+    for (int64_t e = warp; e < total; e += nwarps) {
+        const int gg = (int)(e % g.ng);
+        const int64_t cell = e / g.ng;
+        const int y = (int)(cell % g.ny), x = (int)(cell / g.ny);
+        const Real* base = psi + fidx(x, y, 0, g.ny, h, g.C);
+        double acc = 0.0;
+        for (int n = lane; n < g.nd; n += 32) acc += (double)w[n] * (double)base[n * g.ng + gg];
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+        if (lane == 0) phi[e] = acc;
+    }
+}
+
+// ------------------------------------------------------------------ group source
+template <class Real>
+__global__ void __launch_bounds__(256)
+group_source_kernel(Geo g, const double* phi, const double* ss, const double* src,
+                    const double* fis, double lam, const double* chi, const double* nsf,
+                    Real* q) {
+    const int64_t total = (int64_t)g.nx * g.ny * g.ng;
+    const int G = g.ng;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int b = (int)(e % G);
+        const int64_t cell = e / G;
+        const double* ph = phi + cell * G;
+        const double* s = ss + cell * G * G;
+        double acc = 0.0;
+        for (int aa = 0; aa < G; ++aa) acc += s[aa * G + b] * ph[aa];
+        acc -= s[b * G + b] * ph[b];
+        acc += src[e];
+        if (lam != 0.0) {
+            double prod = 0.0;
+            for (int aa = 0; aa < G; ++aa) prod += nsf[cell * G + aa] * ph[aa];
+            acc += lam * chi[e] * prod;
+        }
+        if (fis) acc += fis[e];
+        q[e] = (Real)acc;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+fission_source_kernel(Geo g, const double* phi, const double* chi, const double* nsf,
+                      double inv_k, double* out) {
+    const int64_t total = (int64_t)g.nx * g.ny * g.ng;
+    const int G = g.ng;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t cell = e / G;
+        double prod = 0.0;
+        for (int aa = 0; aa < G; ++aa) prod += nsf[cell * G + aa] * phi[cell * G + aa];
+        out[e] = inv_k * chi[e] * prod;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+dot_partials_kernel(const double* a, const double* b, int64_t n, double* partials) {
+    __shared__ double red[32];
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        acc += a[i] * b[i];
+    const double t = block_sum(acc, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = t;
+}
+
+// single CTA, fixed order: deterministic
+__global__ void __launch_bounds__(1024)
+sum_f64_kernel(const double* x, int64_t n, double scale, double* out) {
+    __shared__ double red[32];
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += x[i];
+    const double t = block_sum(acc, red);
+    if (threadIdx.x == 0) *out = t * scale;
+}
+
+template <class Real>
+__global__ void __launch_bounds__(256) scale_kernel(Real* x, int64_t n, Real s, int divide) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = divide ? x[i] / s : x[i] * s;
+}
+
+template <class Real>
+__global__ void __launch_bounds__(256)
+sub_interior_kernel(Geo g, Real* psi, int ph, const Real* d, int dh) {
+    const int64_t total = (int64_t)g.nx * g.ny * g.C;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e % g.C);
+        const int64_t cell = e / g.C;
+        const int y = (int)(cell % g.ny), x = (int)(cell / g.ny);
+        psi[fidx(x, y, c, g.ny, ph, g.C)] -= d[fidx(x, y, c, g.ny, dh, g.C)];
+    }
+}
+
+template <class Real>
+__global__ void __launch_bounds__(256)
+ema_kernel(Geo g, Real* avg, int ah, const Real* psi, int ph, Real theta, Real omt, int mode) {
+    const int64_t total = (int64_t)g.nx * g.ny * g.C;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e % g.C);
+        const int64_t cell = e / g.C;
+        const int y = (int)(cell % g.ny), x = (int)(cell / g.ny);
+        const Real p = psi[fidx(x, y, c, g.ny, ph, g.C)];
+        Real* o = avg + fidx(x, y, c, g.ny, ah, g.C);
+        *o = mode == 1 ? p : *o * omt + theta * p;
+    }
+}
+
+// ------------------------------------------------------------------ generic stencils
+// R/grid.py:85-105: out = scale[n] * sum_{a,b} w[a][b] src[i+a-l][j+b-l] on
+// interior +- margin; whole padded output written (zeros elsewhere).
+struct StencilW { double w[121]; };   // up to 11 x 11 taps, passed by value
+
+template <class Real>
+__global__ void __launch_bounds__(256)
+convolve_kernel(Geo g, const Real* src, int h, const StencilW sw, int width, int margin,
+                const Real* scale, Real* out) {
+    const double* w = sw.w;
+    const int NX = g.nx + 2 * h, NY = g.ny + 2 * h;
+    const int l = (width - 1) / 2;
+    const int64_t total = (int64_t)NX * NY * g.C;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e % g.C);
+        const int64_t cell = e / g.C;
+        const int ys = (int)(cell % NY), xs = (int)(cell / NY);
+        const int x = xs - h, y = ys - h;
+        Real acc = Real(0);
+        if (x >= -margin && x < g.nx + margin && y >= -margin && y < g.ny + margin) {
+            for (int aa = 0; aa < width; ++aa)
+                for (int bb = 0; bb < width; ++bb) {
+                    const Real wv = (Real)w[aa * width + bb];
+                    if (wv == Real(0)) continue;
+                    acc += wv * src[((int64_t)(xs + aa - l) * NY + (ys + bb - l)) * g.C + c];
+                }
+            if (scale) acc *= scale[c / g.ng];
+        }
+        out[e] = acc;
+    }
+}
+
+// R/grid.py:108-125: one 1D pass along `axis`, full extent on the other axis.
+template <class Real>
+__global__ void __launch_bounds__(256)
+pass1d_kernel(Geo g, const Real* src, int h, const StencilW sw, int width, int axis,
+              int margin, Real* out) {
+    const double* w = sw.w;
+    const int NX = g.nx + 2 * h, NY = g.ny + 2 * h;
+    const int l = (width - 1) / 2;
+    const int64_t total = (int64_t)NX * NY * g.C;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e % g.C);
+        const int64_t cell = e / g.C;
+        const int ys = (int)(cell % NY), xs = (int)(cell / NY);
+        const int pos = axis == 0 ? xs - h : ys - h;
+        const int next = axis == 0 ? g.nx : g.ny;
+        Real acc = Real(0);
+        if (pos >= -margin && pos < next + margin) {
+            for (int aa = 0; aa < width; ++aa) {
+                const Real wv = (Real)w[aa];
+                if (wv == Real(0)) continue;
+                const int64_t o = axis == 0 ? ((int64_t)(xs + aa - l) * NY + ys)
+                                            : ((int64_t)xs * NY + (ys + aa - l));
+                acc += wv * src[o * g.C + c];
+            }
+        }
+        out[e] = acc;
+    }
+}
+
+}  // namespace csn

@@ -1,0 +1,554 @@
+"""Space-angle sawtooth multigrid on the B200 (R/multigrid.py:1-353).
+
+Each level halves space and (until one patch per face) angle; removal is
+coarsened harmonically.  A cycle forms the finest residual (PG or upwind),
+restricts it through every level (normalised back to lumped-mass units),
+Jacobi-relaxes the correction with the upwind scheme from the coarsest level up
+(prolongation fused into the first sweep of each level), subtracts it, and for
+the PG scheme finishes with relaxations of the full system (the subtraction is
+fused into that sweep).  ``CycleEngine`` owns the device workspaces of one
+hierarchy and issues the kernel sequence; the per-cycle host work is the fp64
+residual read-back that drives ``PGState``.
+"""
+
+import numpy as np
+import torch
+
+from . import _lib
+from .discretisation import (PGConfig, diffusivities_into, jacobi_diagonal, pg_residual_launch,
+                             sigma_tensor, source_tensor)
+from .filters import build_upwind_filters
+from .grid import Field, GridSpec, apply_boundary, default_device
+from .quadrature import N_FACES, coarsen_quadrature
+
+UP_MAX_SWEEPS = 3   # sweeps per temporally blocked smoother launch (csrc/upwind_kernels.cuh)
+
+
+class Level:
+    """One level: grid, ordinates, removal (host fp64) and upwind pieces (R/multigrid.py:32-40)."""
+
+    def __init__(self, grid, quad, sigma_t, upwind, diag=None):
+        self.grid = grid
+        self.quad = quad
+        self.sigma_t = sigma_t
+        self.upwind = upwind
+        self._diag = diag
+        self._dev = {}
+
+    @property
+    def diag(self):
+        """Upwind Jacobi diagonal (device fp64, built on first access only)."""
+        if self._diag is None:
+            self._diag = jacobi_diagonal(self.sigma_t, self.quad, self.grid, "upwind")
+        return self._diag
+
+    def sigma_dev(self, dtype, device):
+        key = ("sigma", dtype, str(device))
+        if key not in self._dev:
+            self._dev[key] = torch.as_tensor(np.ascontiguousarray(self.sigma_t), dtype=dtype,
+                                             device=device)
+        return self._dev[key]
+
+    def consts(self, dtype, device):
+        return self.quad.device(dtype, device, self.grid.dx, self.grid.dy)
+
+    def geom(self, n_group, ghost_w=0, ghost_e=0):
+        g = self.grid
+        return _lib.geom(g.nx, g.ny, self.quad.n_dir, n_group, self.quad.n_a, g.dx, g.dy,
+                         ghost_w, ghost_e)
+
+
+class MultigridHierarchy:
+    """Finest-to-coarsest list of levels."""
+
+    def __init__(self, levels):
+        self.levels = levels
+        self._engines = {}
+
+    @property
+    def n_levels(self):
+        return len(self.levels)
+
+    def __iter__(self):
+        return iter(self.levels)
+
+    def __getitem__(self, i):
+        return self.levels[i]
+
+    def engine(self, n_group, dtype, device):
+        key = (n_group, dtype, str(device))
+        if key not in self._engines:
+            self._engines[key] = CycleEngine(self, n_group, dtype, device)
+        return self._engines[key]
+
+
+def max_levels(nx, ny):
+    """Halve while both extents stay even (R/multigrid.py:60-67)."""
+    n = 1
+    while nx % 2 == 0 and ny % 2 == 0 and nx > 1 and ny > 1:
+        nx //= 2
+        ny //= 2
+        n += 1
+    return n
+
+
+def coarsen_sigma(sigma_t, eps=1e-30):
+    """Harmonic 2x2 average; a zero child forces a zero parent (R/multigrid.py:70-77)."""
+    nx, ny, ng = sigma_t.shape
+    blk = np.asarray(sigma_t).reshape(nx // 2, 2, ny // 2, 2, ng)
+    coarse = 4.0 / (1.0 / np.maximum(blk, eps)).sum(axis=(1, 3))
+    coarse[(blk == 0.0).any(axis=(1, 3))] = 0.0
+    return coarse
+
+
+def build_hierarchy(grid, quad, sigma_t, n_levels=None):
+    """Finest-first levels; angle stops halving at n_a = 1 (R/multigrid.py:80-107)."""
+    if n_levels is None:
+        n_levels = max_levels(grid.nx, grid.ny)
+    if n_levels < 1:
+        raise ValueError("hierarchy needs at least one level")
+    if grid.nx % 2 ** (n_levels - 1) or grid.ny % 2 ** (n_levels - 1):
+        raise ValueError(f"grid {grid.nx}x{grid.ny} not divisible by 2**{n_levels - 1}")
+    levels = []
+    g, q, sig = grid, quad, np.asarray(sigma_t, dtype=np.float64)
+    for i in range(n_levels):
+        levels.append(Level(g, q, sig, build_upwind_filters(g.dx, g.dy)))
+        if i == n_levels - 1:
+            break
+        sig = coarsen_sigma(sig)
+        g = GridSpec(g.nx // 2, g.ny // 2, 2 * g.dx, 2 * g.dy, g.halo)
+        if q.n_a > 1:
+            q = coarsen_quadrature(q)
+    return MultigridHierarchy(levels)
+
+
+def _pair_check(fine_level, coarse_level):
+    fg, cg = fine_level.grid, coarse_level.grid
+    if (cg.nx * 2, cg.ny * 2) != (fg.nx, fg.ny):
+        raise ValueError("levels are not a spatial 2:1 pair")
+    if coarse_level.quad.n_a not in (fine_level.quad.n_a, fine_level.quad.n_a // 2):
+        raise ValueError("levels are not an angular 1:1 or 2:1 pair")
+
+
+def restrict(field, fine_level, coarse_level):
+    """Raw integrated 2x2 (x 2x2 patch) restriction as a coarse Field (R/multigrid.py:110-127)."""
+    _pair_check(fine_level, coarse_level)
+    d = field.data
+    _lib.require_cuda(d)
+    cg = coarse_level.grid
+    out = Field(cg, coarse_level.quad.n_dir, field.n_group, dtype=d.dtype, device=d.device)
+    fc = fine_level.consts(d.dtype, d.device)
+    cc = coarse_level.consts(d.dtype, d.device)
+    _lib.call("csn_restrict", _lib.dtype_code(d), fine_level.geom(field.n_group),
+              coarse_level.geom(field.n_group), _lib.ptr(d), field.grid.halo, _lib.ptr(fc["w"]),
+              _lib.ptr(cc["w"]), 0, _lib.ptr(out.data), cg.halo, _lib.stream())
+    return out
+
+
+def restrict_field_array(arr, fine_level, coarse_level):
+    """Array-in / array-out raw restriction of an interior tensor (R/multigrid.py:342-353)."""
+    _pair_check(fine_level, coarse_level)
+    arr = arr.contiguous()
+    _lib.require_cuda(arr)
+    ng = arr.shape[3]
+    cg = coarse_level.grid
+    out = torch.empty((cg.nx, cg.ny, coarse_level.quad.n_dir, ng), dtype=arr.dtype,
+                      device=arr.device)
+    fc = fine_level.consts(arr.dtype, arr.device)
+    cc = coarse_level.consts(arr.dtype, arr.device)
+    _lib.call("csn_restrict", _lib.dtype_code(arr), fine_level.geom(ng), coarse_level.geom(ng),
+              _lib.ptr(arr), 0, _lib.ptr(fc["w"]), _lib.ptr(cc["w"]), 0, _lib.ptr(out), 0,
+              _lib.stream())
+    return out
+
+
+def prolong(field, coarse_level, fine_level):
+    """Piecewise-constant injection onto the finer level (R/multigrid.py:130-146)."""
+    _pair_check(fine_level, coarse_level)
+    d = field.data
+    _lib.require_cuda(d)
+    fg = fine_level.grid
+    out = Field(fg, fine_level.quad.n_dir, field.n_group, dtype=d.dtype, device=d.device)
+    _lib.call("csn_prolong", _lib.dtype_code(d), coarse_level.geom(field.n_group),
+              fine_level.geom(field.n_group), _lib.ptr(d), field.grid.halo, _lib.ptr(out.data),
+              fg.halo, _lib.stream())
+    return out
+
+
+def _smooth_chain(level, ng, src, per_dof, init, init_mode, init_halo, gc, n_sweeps, scale,
+                  out, out_halo, spare):
+    """Run n_sweeps upwind sweeps in launches of <= 3 (ping-pong through `spare`)."""
+    d = out
+    c = level.consts(d.dtype, d.device)
+    sig = level.sigma_dev(d.dtype, d.device)
+    g = level.geom(ng)
+    dt = _lib.dtype_code(d)
+    first = min(n_sweeps, UP_MAX_SWEEPS)
+    bufs = [out, spare]
+    k = 0
+    _lib.call("csn_upwind_smooth", dt, g, _lib.ptr(src), per_dof, init_mode, _lib.ptr(init),
+              init_halo, gc, _lib.ptr(sig), _lib.ptr(c["mu"]), _lib.ptr(c["nu"]),
+              _lib.ptr(c["strm"]), first, float(scale), _lib.ptr(bufs[0]), out_halo,
+              _lib.stream())
+    done = first
+    while done < n_sweeps:
+        now = min(n_sweeps - done, UP_MAX_SWEEPS)
+        _lib.call("csn_upwind_smooth", dt, g, _lib.ptr(src), per_dof, 1, _lib.ptr(bufs[k]),
+                  out_halo, None, _lib.ptr(sig), _lib.ptr(c["mu"]), _lib.ptr(c["nu"]),
+                  _lib.ptr(c["strm"]), now, float(scale), _lib.ptr(bufs[1 - k]), out_halo,
+                  _lib.stream())
+        k = 1 - k
+        done += now
+    return bufs[k]
+
+
+def jacobi_sweep(psi, q, level, n_sweeps=1, scheme="upwind", cfg=None, fs=None, diag_scale=1.0,
+                 diffusivities=None):
+    """n_sweeps Jacobi relaxations psi <- psi - d^-1 r(psi), in place (R/multigrid.py:149-173).
+
+    The vacuum rule is applied on load before every sweep; psi's halo is
+    refreshed at the end.
+    """
+    cfg = cfg or PGConfig()
+    if scheme not in ("pg", "upwind"):
+        raise ValueError(f"unknown scheme {scheme!r}")
+    d = psi.data
+    _lib.require_cuda(d)
+    g = psi.grid
+    if scheme == "upwind":
+        qt, per_dof = source_tensor(q, g.nx, g.ny, psi.n_dir, psi.n_group, d)
+        if n_sweeps > 0:
+            out = torch.empty_like(d)
+            spare = torch.empty_like(d) if n_sweeps > UP_MAX_SWEEPS else None
+            res = _smooth_chain(level, psi.n_group, qt, per_dof, d, 1, g.halo, None, n_sweeps,
+                                diag_scale, out, g.halo, spare)
+            psi.data = res
+    else:
+        if fs is None:
+            raise ValueError("the pg sweep needs the filter set fs")
+        from .discretisation import pg_anisotropic_diffusivities, _k_tensor
+        for _ in range(n_sweeps):
+            apply_boundary(psi, level.quad)
+            if diffusivities is None:
+                kx, ky = pg_anisotropic_diffusivities(psi, fs, level.quad, cfg)
+            else:
+                kx, ky = (_k_tensor(k, psi.data) for k in diffusivities)
+            out = torch.empty_like(psi.data)
+            pg_residual_launch(psi, level.sigma_t, q, level.quad, fs, kx, ky, g.halo,
+                               psi_out=out, out_halo=g.halo, beta=cfg.beta_diag)
+            psi.data = out
+    apply_boundary(psi, level.quad)
+    return psi
+
+
+# freeze heuristics of the diffusivity Picard iteration (R/multigrid.py:176-182)
+_STALL_WINDOW = 5
+_STALL_FACTOR = 0.9
+_UNFREEZE_GROWTH = 2.0
+_MAX_FREEZE_ATTEMPTS = 3
+
+
+class PGState:
+    """Across-cycle diffusivity Picard state (R/multigrid.py:185-256).
+
+    Host logic is the reference's, decision for decision (``observe``); the
+    averaged iterate and the diffusivities live on the device.  ``log`` records
+    (observe call, "freeze" | "unfreeze") for parity checks.
+    """
+
+    __slots__ = ("diffusivities", "initial_residual", "frozen", "best_residual",
+                 "cycles_since_best", "freeze_residual", "failed_freezes", "avg_theta",
+                 "_avg", "_avg_spare", "_avg_grid", "_avg_quad", "log", "_calls")
+
+    def __init__(self, avg_theta=0.2):
+        self.diffusivities = None
+        self.initial_residual = None
+        self.frozen = False
+        self.best_residual = None
+        self.cycles_since_best = 0
+        self.freeze_residual = None
+        self.failed_freezes = 0
+        self.avg_theta = avg_theta
+        self._avg = None
+        self._avg_spare = None
+        self._avg_grid = None
+        self._avg_quad = None
+        self.log = []
+        self._calls = 0
+
+    @property
+    def psi_avg(self):
+        """The averaged iterate as a Field (halo refreshed on access)."""
+        if self._avg is None:
+            return None
+        f = Field(self._avg_grid, self._avg.shape[2], self._avg.shape[3], self._avg)
+        apply_boundary(f, self._avg_quad)
+        return f
+
+    @psi_avg.setter
+    def psi_avg(self, field):
+        if field is None:
+            self._avg = None
+            return
+        self._avg = field.data
+        self._avg_grid = field.grid
+
+    def averaged_iterate(self, psi, quad=None):
+        """EMA of the iterate (R/multigrid.py:217-225); ``quad`` refreshes the halo."""
+        if self.avg_theta >= 1.0:
+            return psi
+        d = psi.data
+        first = self._avg is None
+        if first:
+            self._avg = torch.empty_like(d)
+            self._avg_grid = psi.grid
+        self._avg_quad = quad if quad is not None else self._avg_quad
+        gm = _lib.geom(psi.grid.nx, psi.grid.ny, psi.n_dir, psi.n_group,
+                       int(round((psi.n_dir / 8) ** 0.5)), psi.grid.dx, psi.grid.dy)
+        _lib.call("csn_ema", _lib.dtype_code(d), gm, _lib.ptr(self._avg), psi.grid.halo,
+                  _lib.ptr(d), psi.grid.halo, float(self.avg_theta), 1 if first else 2,
+                  _lib.stream())
+        if self._avg_quad is None:
+            return Field(psi.grid, psi.n_dir, psi.n_group, self._avg)
+        return self.psi_avg
+
+    def observe(self, resid, k_freeze_rel):
+        self._calls += 1
+        if self.initial_residual is None:
+            self.initial_residual = resid
+            self.best_residual = resid
+            return
+        if self.frozen:
+            if resid > _UNFREEZE_GROWTH * self.freeze_residual:
+                self.frozen = False
+                self.failed_freezes += 1
+                self.best_residual = resid
+                self.cycles_since_best = 0
+                self.log.append((self._calls, "unfreeze"))
+            return
+        if self.failed_freezes >= _MAX_FREEZE_ATTEMPTS:
+            return
+        if resid <= k_freeze_rel * self.initial_residual:
+            self._freeze(resid)
+            return
+        if resid < _STALL_FACTOR * self.best_residual:
+            self.best_residual = resid
+            self.cycles_since_best = 0
+        else:
+            self.cycles_since_best += 1
+            if self.cycles_since_best >= _STALL_WINDOW:
+                self._freeze(resid)
+
+    def _freeze(self, resid):
+        self.frozen = True
+        self.freeze_residual = resid
+        self.cycles_since_best = 0
+        self.log.append((self._calls, "freeze"))
+
+    def scale_average(self, s):
+        """psi_avg /= s (R/eigen.py:246-247)."""
+        if self._avg is not None:
+            _lib.call("csn_scale", _lib.dtype_code(self._avg), _lib.ptr(self._avg),
+                      self._avg.numel(), float(s), 1, _lib.stream())
+
+
+class CycleEngine:
+    """Device workspaces + kernel sequence of one sawtooth cycle on one hierarchy."""
+
+    def __init__(self, hierarchy, n_group, dtype, device):
+        self.h = hierarchy
+        self.ng = n_group
+        self.dtype = dtype
+        self.device = device
+        L = hierarchy.levels
+        self.geoms = [lev.geom(n_group) for lev in L]
+        self.consts = [lev.consts(dtype, device) for lev in L]
+        self.sigma = [lev.sigma_dev(dtype, device) for lev in L]
+        shp = [(lev.grid.nx, lev.grid.ny, lev.quad.n_dir, n_group) for lev in L]
+        e = lambda s: torch.empty(s, dtype=dtype, device=device)
+        self.r0 = e(shp[0])
+        self.src = [self.r0] + [e(s) for s in shp[1:]]
+        self.delta = [e(s) for s in shp]
+        self.spare = [None] * len(L)
+        self.shapes = shp
+        lib = _lib.load()
+        nparts = max(lib.csn_partials_size(_lib.dtype_code(self.r0), g, 3) for g in self.geoms)
+        self.partials = torch.empty(int(nparts), dtype=torch.float64, device=device)
+        self.l1 = torch.zeros(1, dtype=torch.float64, device=device)
+        self.res_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
+        self.psi_alt = None
+        self.k_scratch = None
+        self.probe = None          # {kernel name: [(start event, end event)]} when timing
+
+    def _t0(self):
+        if self.probe is None:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        return ev
+
+    def _t1(self, name, ev0):
+        if ev0 is None:
+            return
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.probe.setdefault(name, []).append((ev0, ev))
+
+    # ---------------------------------------------------------------- correction
+    def correction(self, r0, n_sweeps, finest_scale):
+        """Restrict r0 through the hierarchy, smooth upward; returns the finest delta."""
+        L = self.h.levels
+        dt = _lib.dtype_code(r0)
+        src = [r0] + self.src[1:]
+        for i in range(1, len(L)):
+            _lib.call("csn_restrict", dt, self.geoms[i - 1], self.geoms[i], _lib.ptr(src[i - 1]),
+                      0, _lib.ptr(self.consts[i - 1]["w"]), _lib.ptr(self.consts[i]["w"]), 1,
+                      _lib.ptr(src[i]), 0, _lib.stream())
+        prev = None
+        for i in range(len(L) - 1, -1, -1):
+            scale = finest_scale if i == 0 else 1.0
+            if n_sweeps > UP_MAX_SWEEPS and self.spare[i] is None:
+                self.spare[i] = torch.empty_like(self.delta[i])
+            if prev is None:
+                init, mode, gc = None, 0, None
+            else:
+                init, mode, gc = prev, 2, self.geoms[i + 1]
+            prev = _smooth_chain(L[i], self.ng, src[i], 1, init, mode, 0, gc, n_sweeps, scale,
+                                 self.delta[i], 0, self.spare[i])
+        return prev
+
+    # ---------------------------------------------------------------- cycle
+    def cycle(self, psi, q, fs=None, cfg=None, scheme="pg", n_sweeps=3, pg_sweeps=1,
+              pg_state=None, sync=True):
+        """One sawtooth cycle in place; returns the fp64 L1 of the pre-update residual."""
+        cfg = cfg or PGConfig()
+        L = self.h.levels
+        f = L[0]
+        d = psi.data
+        g = psi.grid
+        dt = _lib.dtype_code(d)
+        c0 = self.consts[0]
+        qt, per_dof = source_tensor(q, g.nx, g.ny, psi.n_dir, psi.n_group, d)
+        if scheme == "pg":
+            if fs is None:
+                raise ValueError("the pg scheme needs the filter set fs")
+            kx, ky = self._diffusivities(psi, fs, cfg, pg_state)
+            t = self._t0()
+            pg_residual_launch(psi, None, None, f.quad, fs, kx, ky, g.halo, r=self.r0, r_halo=0,
+                               partials=self.partials, l1=self.l1, sigma=self.sigma[0], qt=qt,
+                               per_dof=per_dof, consts=c0)
+            self._t1("pg_residual", t)
+        elif scheme == "upwind":
+            t = self._t0()
+            _lib.call("csn_upwind_residual", dt, self.geoms[0], _lib.ptr(d), g.halo,
+                      _lib.ptr(self.sigma[0]), _lib.ptr(qt), per_dof, _lib.ptr(c0["mu"]),
+                      _lib.ptr(c0["nu"]), _lib.ptr(self.r0), 0, _lib.ptr(self.partials),
+                      _lib.ptr(self.l1), _lib.stream())
+            self._t1("upwind_residual", t)
+        else:
+            raise ValueError(f"unknown scheme {scheme!r}")
+        self.res_host.copy_(self.l1, non_blocking=True)
+        t = self._t0()
+        delta = self.correction(self.r0, n_sweeps, cfg.beta_diag if scheme == "pg" else 1.0)
+        self._t1("correction", t)
+        if scheme == "pg" and pg_sweeps > 0:
+            for k in range(pg_sweeps):
+                if self.psi_alt is None or self.psi_alt.shape != d.shape:
+                    self.psi_alt = torch.empty_like(d)
+                out = self.psi_alt
+                t = self._t0()
+                pg_residual_launch(psi, None, None, f.quad, fs, kx, ky, g.halo, psi_out=out,
+                                   out_halo=g.halo, delta=delta if k == 0 else None,
+                                   delta_halo=0, beta=cfg.beta_diag, sigma=self.sigma[0], qt=qt,
+                                   per_dof=per_dof, consts=c0)
+                self._t1("pg_sweep", t)
+                self.psi_alt = psi.data
+                psi.data = out
+        else:
+            _lib.call("csn_sub_interior", dt, self.geoms[0], _lib.ptr(psi.data), g.halo,
+                      _lib.ptr(delta), 0, _lib.stream())
+        t = self._t0()
+        apply_boundary(psi, f.quad)
+        self._t1("boundary", t)
+        if not sync:
+            return None
+        torch.cuda.current_stream().synchronize()
+        res = float(self.res_host[0])
+        if scheme == "pg" and pg_state is not None:
+            pg_state.observe(res, cfg.k_freeze_rel)
+        return res
+
+    def _diffusivities(self, psi, fs, cfg, pg_state):
+        d = psi.data
+        g = psi.grid
+        c0 = self.consts[0]
+        l = fs.half_width
+        if g.halo < 3 * l:
+            raise ValueError(f"PG diffusivities need halo >= {3 * l}, field has {g.halo}")
+        nd, ng, na = psi.n_dir, psi.n_group, self.h.levels[0].quad.n_a
+        if pg_state is None:
+            if self.k_scratch is None or self.k_scratch[0].shape != d.shape:
+                self.k_scratch = (torch.zeros_like(d), torch.zeros_like(d))
+            kx, ky = self.k_scratch
+            diffusivities_into(d, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky, g.halo)
+            return kx, ky
+        need_k = pg_state.diffusivities is None or not pg_state.frozen
+        if need_k and pg_state.diffusivities is None:
+            pg_state.diffusivities = (torch.zeros_like(d), torch.zeros_like(d))
+        kx, ky = pg_state.diffusivities
+        if pg_state.avg_theta >= 1.0:
+            if need_k:
+                diffusivities_into(d, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky, g.halo)
+            return kx, ky
+        pg_state._avg_quad = self.h.levels[0].quad
+        first = pg_state._avg is None
+        if first:
+            pg_state._avg = torch.empty_like(d)
+            pg_state._avg_grid = g
+        t = self._t0()
+        if need_k:
+            if first:
+                diffusivities_into(d, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky, g.halo,
+                                   avg_out=pg_state._avg, avg_mode=1)
+            else:
+                if pg_state._avg_spare is None or pg_state._avg_spare.shape != d.shape:
+                    pg_state._avg_spare = torch.empty_like(d)
+                out = pg_state._avg_spare
+                diffusivities_into(d, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky, g.halo,
+                                   avg_in=pg_state._avg, avg_out=out, avg_mode=2,
+                                   theta=pg_state.avg_theta)
+                pg_state._avg_spare = pg_state._avg
+                pg_state._avg = out
+        else:
+            _lib.call("csn_ema", _lib.dtype_code(d), self.geoms[0], _lib.ptr(pg_state._avg),
+                      g.halo, _lib.ptr(d), g.halo, float(pg_state.avg_theta), 1 if first else 2,
+                      _lib.stream())
+        self._t1("pg_diffusivity" if need_k else "ema", t)
+        return kx, ky
+
+
+def sawtooth_cycle(psi, q, hierarchy, fs=None, cfg=None, scheme="pg", n_sweeps=3, pg_sweeps=1,
+                   pg_state=None):
+    """One sawtooth iteration; returns (psi, finest residual L1) (R/multigrid.py:259-306)."""
+    _lib.require_cuda(psi.data)
+    eng = hierarchy.engine(psi.n_group, psi.data.dtype, psi.data.device)
+    res = eng.cycle(psi, q, fs, cfg, scheme, n_sweeps, pg_sweeps, pg_state)
+    return psi, res
+
+
+def mg_correction(residual_interior, hierarchy, n_sweeps=3, finest_diag_scale=1.0, cfg=None):
+    """Restrict a finest residual and smooth the correction upward (R/multigrid.py:309-339).
+
+    Returns the finest correction as a Field (to be subtracted).
+    """
+    r = residual_interior
+    if not isinstance(r, torch.Tensor):
+        r = torch.as_tensor(np.asarray(r), device=default_device())
+    r = r.contiguous()
+    _lib.require_cuda(r)
+    eng = hierarchy.engine(r.shape[3], r.dtype, r.device)
+    delta = eng.correction(r, n_sweeps, finest_diag_scale)
+    f = hierarchy[0]
+    out = Field(f.grid, f.quad.n_dir, r.shape[3], dtype=r.dtype, device=r.device)
+    out.interior.copy_(delta)
+    return out

@@ -1,0 +1,152 @@
+"""Octahedral discrete-ordinates quadrature (host setup, float64).
+
+Same ordinate set as R/quadrature.py:112-176: eight octahedron faces, each an
+``n_a x n_a`` grid of planar patches projected radially onto the unit sphere;
+weight = spherical patch area, direction = patch mean of the unit vector, both in
+closed form (spherical-triangle solid angles; half the arc-angle-weighted sum of
+great-circle axes for the moment).  Storage is face-major, then row (equator ->
+pole), then column, so 2x2 angle coarsening is a reshape.  Computed here for all
+patches at once (vectorised over the patch axis) and uploaded once per level.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+FOUR_PI = 4.0 * np.pi
+N_FACES = 8
+OCTANT_SIGNS = ((1, 1, 1), (-1, 1, 1), (-1, -1, 1), (1, -1, 1),
+                (1, 1, -1), (-1, 1, -1), (-1, -1, -1), (1, -1, -1))
+
+
+@dataclass(frozen=True, eq=False)
+class AngularQuadrature:
+    """Ordinate set: mean directions, patch weights and face membership."""
+
+    n_a: int
+    directions: np.ndarray   # (n_dir, 3): mu, nu, xi
+    weights: np.ndarray      # (n_dir,), sum 4 pi
+    face_index: np.ndarray   # (n_dir,)
+
+    def __post_init__(self):
+        for arr in (self.directions, self.weights, self.face_index):
+            arr.setflags(write=False)
+
+    @property
+    def n_faces(self):
+        return N_FACES
+
+    @property
+    def n_dir(self):
+        return self.weights.shape[0]
+
+    @property
+    def mu(self):
+        return self.directions[:, 0]
+
+    @property
+    def nu(self):
+        return self.directions[:, 1]
+
+    @property
+    def xi(self):
+        return self.directions[:, 2]
+
+    def device(self, dtype, device, dx=None, dy=None):
+        """Cached device copies: mu, nu, w (and |mu|/dx + |nu|/dy when dx, dy given)."""
+        import torch
+        cache = self.__dict__.setdefault("_dev", {})
+        key = (str(dtype), str(device), dx, dy)
+        if key not in cache:
+            up = lambda a: torch.tensor(np.array(a), dtype=dtype, device=device)
+            d = {"mu": up(self.mu), "nu": up(self.nu), "w": up(self.weights)}
+            if dx is not None:
+                strm = np.abs(self.mu) / dx + np.abs(self.nu) / dy
+                d["strm"] = up(strm)
+            cache[key] = d
+        return cache[key]
+
+
+def _cross(a, b):
+    return np.cross(a, b)
+
+
+def _dot(a, b):
+    return np.einsum("...i,...i->...", a, b)
+
+
+def _patch_area_moment(p):
+    """Area and moment of spherical quads p[k, 4, 3] (unit corners, cyclic order).
+
+    Degenerate (pole) edges have zero length and drop out of both sums.
+    """
+    a, b, c, d = p[:, 0], p[:, 1], p[:, 2], p[:, 3]
+
+    def tri(u, v, w):
+        num = np.abs(_dot(u, _cross(v, w)))
+        den = 1.0 + _dot(u, v) + _dot(v, w) + _dot(w, u)
+        return 2.0 * np.arctan2(num, den)
+
+    area = tri(a, b, c) + tri(a, c, d)
+    mom = np.zeros_like(a)
+    for u, v in ((a, b), (b, c), (c, d), (d, a)):
+        ax = _cross(u, v)
+        s = np.linalg.norm(ax, axis=1)
+        ok = s >= 1e-15
+        ang = np.arctan2(s, _dot(u, v))
+        mom[ok] += (ang[ok] / s[ok])[:, None] * ax[ok]
+    mom *= 0.5
+    flip = _dot(mom, p.mean(axis=1)) < 0.0
+    mom[flip] = -mom[flip]
+    return area, mom
+
+
+def build_quadrature(n_a):
+    """``8 n_a^2`` ordinates with weights rescaled to sum to 4 pi (R/quadrature.py:112-151)."""
+    if not isinstance(n_a, (int, np.integer)) or n_a < 1 or (n_a & (n_a - 1)) != 0:
+        raise ValueError(f"n_a must be a positive power of 2, got {n_a!r}")
+    n_a = int(n_a)
+    k = np.arange(n_a, dtype=float)
+    t0, t1 = k / n_a, (k + 1) / n_a          # rows towards the pole
+    s0, s1 = k / n_a, (k + 1) / n_a          # columns along the equator edge
+    dirs, wts = [], []
+    for sx, sy, sz in OCTANT_SIGNS:
+        va = np.array([sx, 0.0, 0.0])
+        vb = np.array([0.0, sy, 0.0])
+        vp = np.array([0.0, 0.0, sz])
+
+        def pt(s, t):
+            s = s[None, :, None]
+            t = t[:, None, None]
+            return (1.0 - t) * ((1.0 - s) * va + s * vb) + t * vp
+
+        corners = np.stack([pt(s0, t0), pt(s1, t0), pt(s1, t1), pt(s0, t1)], axis=2)
+        corners = corners.reshape(n_a * n_a, 4, 3)
+        corners = corners / np.linalg.norm(corners, axis=2, keepdims=True)
+        area, mom = _patch_area_moment(corners)
+        wts.append(area)
+        dirs.append(mom / area[:, None])
+    weights = np.concatenate(wts)
+    directions = np.concatenate(dirs)
+    weights = weights * (FOUR_PI / weights.sum())
+    return AngularQuadrature(n_a=n_a, directions=directions, weights=weights,
+                             face_index=np.repeat(np.arange(N_FACES), n_a * n_a))
+
+
+def coarsen_quadrature(quad):
+    """Merge 2x2 patch blocks per face: weights add, directions weight-average."""
+    if quad.n_a < 2:
+        raise ValueError("cannot coarsen: already at one patch per face")
+    m = quad.n_a // 2
+    w = quad.weights.reshape(N_FACES, m, 2, m, 2)
+    d = quad.directions.reshape(N_FACES, m, 2, m, 2, 3)
+    wc = w.sum(axis=(2, 4))
+    dc = (d * w[..., None]).sum(axis=(2, 4)) / wc[..., None]
+    return AngularQuadrature(n_a=m, directions=dc.reshape(-1, 3), weights=wc.reshape(-1),
+                             face_index=np.repeat(np.arange(N_FACES), m * m))
+
+
+def quadrature_to_csv(quad, stream):
+    stream.write("mu,nu,xi,weight,face\n")
+    for (mu, nu, xi), w, f in zip(quad.directions, quad.weights, quad.face_index):
+        stream.write(f"{mu:.17g},{nu:.17g},{xi:.17g},{w:.17g},{int(f)}\n")
