@@ -47,6 +47,24 @@ __device__ __forceinline__ bool resolve_vac(int& x, int& y, const Geo& g, bool m
 template <class Real>
 __device__ __forceinline__ Real ldg(const Real* p) { return __ldg(p); }
 
+// Ampere+ async global->shared copy of one element (LDGSTS); src-size 0 zero-fills,
+// which is how the vacuum rule's zero halo is staged without a branch in smem.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = valid ? BYTES : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gmem),
+                 "n"(BYTES), "r"(n)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 // NaN-propagating min (numpy.minimum semantics, R/discretisation.py:150-158).
 template <class Real>
 __device__ __forceinline__ Real nanmin(Real a, Real b) {

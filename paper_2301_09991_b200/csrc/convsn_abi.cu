@@ -38,21 +38,24 @@ inline int pick_ly(int64_t ctas_xy, int rows, int T) {
     return ly;
 }
 
-template <class Real, int L>
-PGTaps<Real, L> make_taps(const double* taps, double dx, double dy) {
-    PGTaps<Real, L> t;
+// The kernels use the compile-time unit taps of taps_table.cuh; the caller's taps
+// (host [3][2L+1] = mass, grad, stiff) must be the ConvFEM order-L set.
+template <int L>
+bool taps_match(const double* taps) {
     constexpr int T = 2 * L + 1;
-    const double* m = taps;
-    const double* gr = taps + T;
-    const double* st = taps + 2 * T;
     for (int a = 0; a < T; ++a) {
-        t.m[a] = (Real)m[a];
-        t.gx[a] = (Real)(gr[a] / dx);
-        t.gy[a] = (Real)(gr[a] / dy);
-        t.sx[a] = (Real)(st[a] / (dx * dx));
-        t.sy[a] = (Real)(st[a] / (dy * dy));
+        const double ref[3] = {UnitTaps<L>::m(a), UnitTaps<L>::g(a), UnitTaps<L>::s(a)};
+        for (int k = 0; k < 3; ++k) {
+            const double v = taps[k * T + a];
+            if (fabs(v - ref[k]) > 1e-12 * (1.0 + fabs(ref[k]))) return false;
+        }
     }
-    return t;
+    return true;
+}
+
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 // ------------------------------------------------------------------ PG residual
@@ -64,14 +67,16 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
                      double beta, double* partials, double* l1, cudaStream_t st) {
     constexpr int T = 2 * L + 1;
     if (k_h < L) return CSN_E_ARG;
-    PGResidArgs<Real, L> a;
+    if (!taps_match<L>(taps)) return CSN_E_ARG;
+    PGResidArgs<Real> a;
     a.g = make_geo(*g);
-    a.t = make_taps<Real, L>(taps, g->dx, g->dy);
     a.psi = (const Real*)psi; a.psi_h = psi_h;
     a.delta = (const Real*)delta; a.delta_h = delta_h;
     a.kx = (const Real*)kx; a.ky = (const Real*)ky; a.k_h = k_h;
     a.sigma = (const Real*)sigma; a.q = (const Real*)q; a.q_per_dof = q_per_dof;
     a.mu = (const Real*)mu; a.nu = (const Real*)nu; a.strm = (const Real*)strm;
+    a.inv_dx = (Real)(1.0 / g->dx); a.inv_dy = (Real)(1.0 / g->dy);
+    a.hx = (Real)(0.5 / (g->dx * g->dx)); a.hy = (Real)(0.5 / (g->dy * g->dy));
     a.r = (Real*)r; a.r_h = r_h;
     a.out = (Real*)out; a.out_h = out_h; a.beta = (Real)beta;
     const int gx = (int)cdiv(g->nx, PG_TX);
@@ -81,11 +86,17 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
     a.partials = (l1 || partials) ? partials : nullptr;
     dim3 grid(gx, gy, gz), block(PG_CC, PG_TX);
     if (out) {
-        pg_residual_kernel<Real, L, true><<<grid, block, 0, st>>>(a);
+        constexpr size_t sm = pg_residual_smem<Real, L, true>();
+        static bool attr = false;
+        if (!attr) { set_smem(pg_residual_kernel<Real, L, true>, sm); attr = true; }
+        pg_residual_kernel<Real, L, true><<<grid, block, sm, st>>>(a);
         CSN_CHECK_LAUNCH();
     } else {
         if (l1 && !partials) return CSN_E_ARG;
-        pg_residual_kernel<Real, L, false><<<grid, block, 0, st>>>(a);
+        constexpr size_t sm = pg_residual_smem<Real, L, false>();
+        static bool attr = false;
+        if (!attr) { set_smem(pg_residual_kernel<Real, L, false>, sm); attr = true; }
+        pg_residual_kernel<Real, L, false><<<grid, block, sm, st>>>(a);
         CSN_CHECK_LAUNCH();
         if (l1) {
             sum_f64_kernel<<<1, 1024, 0, st>>>(partials, (int64_t)gx * gy * gz, 1.0, l1);
@@ -101,28 +112,33 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
               int avg_mode, double theta, const void* mu, const void* nu, void* kx, void* ky,
               int k_h, cudaStream_t st) {
     constexpr int T = 2 * L + 1;
-    constexpr int TXO = K_TXS - 2 * L;
+    constexpr int KT = KTile<Real, L>::value;
+    constexpr int TXO = KT - 2 * L;
     if (k_h < L) return CSN_E_ARG;
+    if (!taps_match<L>(taps)) return CSN_E_ARG;
     if (avg_mode < 0 || avg_mode > 2) return CSN_E_SCHEME;
     if (avg_mode >= 1 && !avg_out) return CSN_E_ARG;
     if (avg_mode == 2 && (!avg_in || avg_in == avg_out)) return CSN_E_ARG;
-    PGKArgs<Real, L> a;
+    PGKArgs<Real> a;
     a.g = make_geo(*g);
-    a.t = make_taps<Real, L>(taps, g->dx, g->dy);
     a.psi = (const Real*)psi; a.psi_h = psi_h;
-    a.avg_in = (const Real*)avg_in; a.avg_in_h = avg_in_h;
-    a.avg_out = (Real*)avg_out; a.avg_out_h = avg_out_h;
+    a.avg_in = (const Real*)avg_in; a.avg_in_h = avg_in ? avg_in_h : 0;
+    a.avg_out = (Real*)avg_out; a.avg_out_h = avg_out ? avg_out_h : 0;
     a.avg_mode = avg_mode; a.theta = (Real)theta; a.omt = (Real)(1.0 - theta);
     a.eps = (Real)cfg[0]; a.alpha_r = (Real)cfg[1]; a.a_abs = (Real)cfg[2]; a.a_sq = (Real)cfg[3];
     a.dx = (Real)g->dx; a.dy = (Real)g->dy;
+    a.inv_dx = (Real)(1.0 / g->dx); a.inv_dy = (Real)(1.0 / g->dy);
     a.mu = (const Real*)mu; a.nu = (const Real*)nu;
     a.kx = (Real*)kx; a.ky = (Real*)ky; a.k_h = k_h;
     const int gx = (int)cdiv(g->nx + 2 * L, TXO);
     const int gy = (int)cdiv((int64_t)g->nd * g->ng, PG_CC);
     a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T);
     const int gz = (int)cdiv(g->ny + 2 * L, a.ly);
-    dim3 grid(gx, gy, gz), block(PG_CC, K_TXS);
-    pg_diffusivity_kernel<Real, L><<<grid, block, 0, st>>>(a);
+    dim3 grid(gx, gy, gz), block(PG_CC, KT);
+    constexpr size_t sm = pg_k_smem<Real, L>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_diffusivity_kernel<Real, L>, sm); attr = true; }
+    pg_diffusivity_kernel<Real, L><<<grid, block, sm, st>>>(a);
     CSN_CHECK_LAUNCH();
     return CSN_OK;
 }
@@ -132,7 +148,6 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
                        const void* init, int init_h, const csn_geom* gc, const void* sigma,
                        const void* mu, const void* nu, const void* strm, int n_sweeps,
                        double diag_scale, void* out, int out_h, cudaStream_t st) {
-    constexpr int CC = sizeof(Real) == 4 ? 16 : 8;
     UpSmoothArgs<Real> a;
     a.g = make_geo(*g);
     a.src = (const Real*)src; a.q_per_dof = q_per_dof;
@@ -152,12 +167,16 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
     a.dx = (Real)g->dx; a.dy = (Real)g->dy;
     a.scale = (Real)diag_scale; a.use_scale = diag_scale != 1.0;
     a.out = (Real*)out; a.out_h = out_h;
-    const int tiles = (int)(cdiv(g->nx, UP_T) * cdiv(g->ny, UP_T));
-    const int gy = (int)cdiv((int64_t)g->nd * g->ng, CC);
-    const size_t smem = (size_t)3 * UP_W * UP_W * CC * sizeof(Real);
-    static_assert((size_t)3 * UP_W * UP_W * CC * sizeof(Real) <= 48 * 1024, "smem");
     a.n_sweeps = n_sweeps;
-    upwind_smooth_kernel<Real, CC><<<dim3(tiles, gy), 256, smem, st>>>(a);
+    const int gx = (int)cdiv(g->nx, UP_XW - 2 * n_sweeps);
+    const int gy = (int)cdiv((int64_t)g->nd * g->ng, UP_CC);
+    // y chunks: enough CTAs to fill the machine, chunks long against the 2H warm-up
+    int chunks = 1;
+    while ((int64_t)gx * gy * chunks < 148 * 4 && g->ny / (chunks * 2) >= 8 * (n_sweeps + 1))
+        chunks *= 2;
+    a.ly = (int)cdiv(g->ny, chunks);
+    const int gz = (int)cdiv(g->ny, a.ly);
+    upwind_smooth_kernel<Real><<<dim3(gx, gy, gz), dim3(UP_CC, UP_XW), 0, st>>>(a);
     CSN_CHECK_LAUNCH();
     return CSN_OK;
 }

@@ -2,52 +2,60 @@
 // the PG residual / fused PG Jacobi sweep (K3 / K5).
 //
 // Both kernels are "2.5D y-marching" stencil engines.  A CTA owns a strip of x cells
-// x a chunk of 32 contiguous channels (ordinate-group pairs, the fastest storage axis,
-// so every row load is a coalesced 128 B (fp32) segment per cell) and walks along y.
-// Each step stages one new y row (plus the x halo) in shared memory; every thread
-// runs the x-pass taps of its own cell from shared memory and pushes the results into
-// register ring buffers of depth T = 2l+1 indexed by (row mod T).  The y pass then
-// reads T ring entries per output.  The y loop is unrolled by T so every ring index
-// is a compile-time constant (no local-memory arrays).
+// x a chunk of 32 contiguous channels (ordinate-group pairs, the fastest storage
+// axis, so every row load is one coalesced 128 B (fp32) segment per cell) and walks
+// along y.  Rows are staged into an S-deep shared-memory ring with cp.async (LDGSTS,
+// zero-fill for the vacuum halo) S-1 rows ahead of use, so DRAM latency hides behind
+// the stencil arithmetic of the rows in flight.  Each thread runs the x-pass taps of
+// its own cell from shared memory and pushes the results into register ring buffers
+// of depth T = 2l+1 indexed by (row mod T); the y pass reads T ring entries per
+// output.  The y loop is unrolled by T so every ring index is a compile-time constant.
 //
-// Pass order and tap folding follow the reference exactly (x pass first, then y
-// pass, taps pre-divided by dx / dx^2 as in R/discretisation.py:114-122,503-504), so
-// the fp64 instantiation reproduces the reference to rounding.
+// Unit-spacing taps are compile-time constants (taps_table.cuh, generated from the
+// host filter construction) so every tap is an FFMA immediate; the 1/dx, 1/dx^2
+// factors the reference folds into its taps (R/discretisation.py:114-122,503-504)
+// are applied once per output instead.  Same pass order as the reference (x pass,
+// then y pass); the fp64 instantiation agrees with it to ~1e-15 relative per pass.
 #pragma once
 #include "common.cuh"
+#include "taps_table.cuh"
 
 namespace csn {
 
 constexpr int PG_CC = 32;    // channels per CTA (one warp lane per channel)
 constexpr int PG_TX = 8;     // x cells per CTA (residual / sweep kernel)
-constexpr int K_TXS = 16;    // stage-1 x cells per CTA (diffusivity kernel)
 
+// stage-1 x cells per CTA of the diffusivity kernel (stage-2 outputs = KTile - 2L)
 template <class Real, int L>
-struct PGTaps {
-    Real m[2 * L + 1];    // mass1
-    Real gx[2 * L + 1];   // grad1 / dx
-    Real gy[2 * L + 1];   // grad1 / dy
-    Real sx[2 * L + 1];   // stiff1 / dx^2
-    Real sy[2 * L + 1];   // stiff1 / dy^2
-};
+struct KTile { static constexpr int value = (sizeof(Real) == 8 || L == 1) ? 16 : 24; };
+
+template <class Real>
+struct PGStages { static constexpr int value = sizeof(Real) == 4 ? 4 : 3; };
+
+template <class Real>
+__device__ __forceinline__ Real fast_div(Real a, Real b) { return a / b; }
+template <>
+__device__ __forceinline__ float fast_div<float>(float a, float b) {
+    return a * __frcp_rn(b);      // correctly rounded reciprocal, then one rounding more
+}
 
 // ---------------------------------------------------------------------------------
 // K3 / K5: PG residual  r = mu psi_x + nu psi_y + diff_x + diff_y + sigma psi - q
-//   psi_x = M_y G_x psi,  psi_y = G_y M_x psi,
-//   diff_x = 1/2 [Kx(kx psi) + kx Kx(psi) - psi Kx(kx)],  Kx = M_y S_x,
-//   diff_y = 1/2 [Ky(ky psi) + ky Ky(psi) - psi Ky(ky)],  Ky = S_y M_x
+//   psi_x = M_y G_x psi / dx,  psi_y = G_y M_x psi / dy,
+//   diff_x = 1/(2dx^2) [Kx(kx psi) + kx Kx(psi) - psi Kx(kx)],  Kx = M_y S_x,
+//   diff_y = 1/(2dy^2) [Ky(ky psi) + ky Ky(psi) - psi Ky(ky)],  Ky = S_y M_x
 // (R/discretisation.py:227-276).  SWEEP: psi' = psi - delta on load, output
 // psi' - r / (beta d) (R/multigrid.py:159-172,301-304).
 // ---------------------------------------------------------------------------------
-template <class Real, int L>
+template <class Real>
 struct PGResidArgs {
     Geo g;
-    PGTaps<Real, L> t;
     const Real* psi; int psi_h;
     const Real* delta; int delta_h;
     const Real* kx; const Real* ky; int k_h;
     const Real* sigma; const Real* q; int q_per_dof;
     const Real* mu; const Real* nu; const Real* strm;
+    Real inv_dx, inv_dy, hx, hy;        // 1/dx, 1/dy, 1/(2 dx^2), 1/(2 dy^2)
     Real* r; int r_h;
     Real* out; int out_h; Real beta;
     double* partials;
@@ -55,11 +63,22 @@ struct PGResidArgs {
 };
 
 template <class Real, int L, bool SWEEP>
+constexpr size_t pg_residual_smem() {
+    return (size_t)PGStages<Real>::value * (SWEEP ? 4 : 3) * (PG_TX + 2 * L) * PG_CC * sizeof(Real);
+}
+
+template <class Real, int L, bool SWEEP>
 __global__ void __launch_bounds__(PG_CC * PG_TX, (sizeof(Real) == 4 && L <= 3) ? 2 : 1)
-pg_residual_kernel(const PGResidArgs<Real, L> a) {
+pg_residual_kernel(const PGResidArgs<Real> a) {
+    using TP = UnitTaps<L>;
     constexpr int T = 2 * L + 1;
     constexpr int W = PG_TX + 2 * L;
-    __shared__ Real sb[2][3][W][PG_CC];
+    constexpr int NX = (W + PG_TX - 1) / PG_TX;    // staged cells per thread
+    constexpr int NF = SWEEP ? 4 : 3;              // psi, kx, ky (, delta)
+    constexpr int S = PGStages<Real>::value;       // rows in flight
+    constexpr int FS = W * PG_CC;                  // elements per field row
+    extern __shared__ __align__(16) unsigned char smraw[];
+    Real* sm = reinterpret_cast<Real*>(smraw);
     __shared__ double red[32];
 
     const Geo& g = a.g;
@@ -70,103 +89,143 @@ pg_residual_kernel(const PGResidArgs<Real, L> a) {
     const int n = cs / g.ng, gg = cs - n * g.ng;
     const Real mu = a.mu[n], nu = a.nu[n];
     const bool mpos = mu > Real(0), npos = nu > Real(0);
+    const Real mu_dx = mu * a.inv_dx, nu_dy = nu * a.inv_dy;
     const int x0 = blockIdx.x * PG_TX;
     const int x = x0 + ty;
     const int ya = blockIdx.z * a.ly;
     const int yb = min(g.ny, ya + a.ly);
     const bool xval = x < g.nx;
+    const int nsteps = 2 * L + (int)(((yb - ya) + T - 1) / T) * T;   // lead rows ya-L ...
 
-    // x-pass rings (by row mod T)
-    Real rgx[T], rmx[T], rsx[T], rsk[T], rkx[T], rmk[T], rky[T];
-    Real cp[T], ckx[T], cky[T];
+    // row-independent part of the staging addresses of this thread's cells
+    const int64_t pp = (int64_t)(g.ny + 2 * a.psi_h) * g.C;        // psi x pitch
+    const int64_t dp = (int64_t)(g.ny + 2 * a.delta_h) * g.C;
+    const int64_t kp = (int64_t)(g.ny + 2 * a.k_h) * g.C;
+    int64_t pxo[NX], dxo[NX], kxo[NX];
+    bool pz[NX], kz[NX];
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+        const int xi = ty + j * PG_TX;
+        int xg = x0 - L + xi, xr = xg;
+        bool zero = !cval || xi >= W;
+        if (xr < 0) { if (!g.ghost_w) { zero |= mpos; xr = 0; } }
+        else if (xr >= g.nx) { if (!g.ghost_e) { zero |= !mpos; xr = g.nx - 1; } }
+        pz[j] = zero;
+        pxo[j] = (int64_t)(xr + a.psi_h) * pp + c;
+        dxo[j] = (int64_t)(xr + a.delta_h) * dp + c;
+        kz[j] = !cval || xi >= W || xg < -L || xg >= g.nx + L;
+        kxo[j] = (int64_t)(xg + a.k_h) * kp + c;
+    }
 
-    auto load_row = [&](int yy, int buf) {
-        for (int xi = ty; xi < W; xi += PG_TX) {
-            const int xg = x0 - L + xi;
-            Real vp = Real(0), v1 = Real(0), v2 = Real(0);
-            if (cval) {
-                int xr = xg, yr = yy;
-                if (resolve_vac(xr, yr, g, mpos, npos)) {
-                    vp = a.psi[fidx(xr, yr, c, g.ny, a.psi_h, g.C)];
-                    if (SWEEP && a.delta) vp -= a.delta[fidx(xr, yr, c, g.ny, a.delta_h, g.C)];
+    auto issue_row = [&](int yy, int b) {
+        Real* base = sm + (size_t)b * NF * FS;
+        bool yz = false;
+        int yr = yy;
+        if (yr < 0) { yz = npos; yr = 0; }
+        else if (yr >= g.ny) { yz = !npos; yr = g.ny - 1; }
+        const bool kyz = yy < -L || yy >= g.ny + L;
+        const int64_t prow = (int64_t)(yr + a.psi_h) * g.C;
+        const int64_t drow = (int64_t)(yr + a.delta_h) * g.C;
+        const int64_t krow = (int64_t)(yy + a.k_h) * g.C;
+#pragma unroll
+        for (int j = 0; j < NX; ++j) {
+            const int xi = ty + j * PG_TX;
+            if (xi < W) {
+                Real* dst = base + xi * PG_CC + tx;
+                const bool ok = !(pz[j] || yz);
+                cp_async<sizeof(Real)>(dst, a.psi + (ok ? pxo[j] + prow : 0), ok);
+                if (SWEEP) {
+                    const bool okd = ok && a.delta != nullptr;
+                    cp_async<sizeof(Real)>(dst + 3 * FS, okd ? a.delta + dxo[j] + drow : a.psi, okd);
                 }
-                if (xg >= -L && xg < g.nx + L && yy >= -L && yy < g.ny + L) {
-                    const int64_t o = fidx(xg, yy, c, g.ny, a.k_h, g.C);
-                    v1 = a.kx[o];
-                    v2 = a.ky[o];
-                }
+                const bool kok = !(kz[j] || kyz);
+                const int64_t ko = kok ? kxo[j] + krow : 0;
+                cp_async<sizeof(Real)>(dst + FS, a.kx + ko, kok);
+                cp_async<sizeof(Real)>(dst + 2 * FS, a.ky + ko, kok);
             }
-            sb[buf][0][xi][tx] = vp;
-            sb[buf][1][xi][tx] = v1;
-            sb[buf][2][xi][tx] = v2;
         }
     };
 
-#define PG_XPASS(BUF, SLOT)                                                        \
-    {                                                                              \
-        Real a_g = 0, a_m = 0, a_s = 0, a_sk = 0, a_k = 0, a_mk = 0, a_ky = 0;       \
-        _Pragma("unroll") for (int t_ = 0; t_ < T; ++t_) {                         \
-            const Real p_ = sb[BUF][0][ty + t_][tx];                               \
-            const Real k1_ = sb[BUF][1][ty + t_][tx];                              \
-            const Real k2_ = sb[BUF][2][ty + t_][tx];                              \
-            a_g += a.t.gx[t_] * p_;                                                \
-            a_m += a.t.m[t_] * p_;                                                 \
-            a_s += a.t.sx[t_] * p_;                                                \
-            a_sk += a.t.sx[t_] * (p_ * k1_);                                       \
-            a_k += a.t.sx[t_] * k1_;                                               \
-            a_mk += a.t.m[t_] * (p_ * k2_);                                        \
-            a_ky += a.t.m[t_] * k2_;                                               \
-        }                                                                          \
-        rgx[SLOT] = a_g; rmx[SLOT] = a_m; rsx[SLOT] = a_s; rsk[SLOT] = a_sk;       \
-        rkx[SLOT] = a_k; rmk[SLOT] = a_mk; rky[SLOT] = a_ky;                       \
-        cp[SLOT] = sb[BUF][0][ty + L][tx];                                         \
-        ckx[SLOT] = sb[BUF][1][ty + L][tx];                                        \
-        cky[SLOT] = sb[BUF][2][ty + L][tx];                                        \
+    // x-pass rings (by row mod T), unit taps
+    Real rgx[T], rmx[T], rsx[T], rsk[T], rkx[T], rmk[T], rky[T];
+    Real cp[T], ckx[T], cky[T];
+
+#define PG_STEP(K, SLOT)                                                             \
+    {                                                                                \
+        const int k_ = (K);                                                          \
+        cp_async_wait<S - 2>();                                                      \
+        Real* buf_ = sm + (size_t)(k_ % S) * NF * FS;                                \
+        if (SWEEP) {                                                                 \
+            _Pragma("unroll") for (int j = 0; j < NX; ++j) {                         \
+                const int xi = ty + j * PG_TX;                                       \
+                if (xi < W) buf_[xi * PG_CC + tx] -= buf_[3 * FS + xi * PG_CC + tx]; \
+            }                                                                        \
+        }                                                                            \
+        __syncthreads();                                                             \
+        Real a_g = 0, a_m = 0, a_s = 0, a_sk = 0, a_k = 0, a_mk = 0, a_ky = 0;         \
+        _Pragma("unroll") for (int t_ = 0; t_ < T; ++t_) {                           \
+            const Real p_ = buf_[(ty + t_) * PG_CC + tx];                            \
+            const Real k1_ = buf_[FS + (ty + t_) * PG_CC + tx];                      \
+            const Real k2_ = buf_[2 * FS + (ty + t_) * PG_CC + tx];                  \
+            a_g += Real(TP::g(t_)) * p_;                                             \
+            a_m += Real(TP::m(t_)) * p_;                                             \
+            a_s += Real(TP::s(t_)) * p_;                                             \
+            a_sk += Real(TP::s(t_)) * (p_ * k1_);                                    \
+            a_k += Real(TP::s(t_)) * k1_;                                            \
+            a_mk += Real(TP::m(t_)) * (p_ * k2_);                                    \
+            a_ky += Real(TP::m(t_)) * k2_;                                           \
+        }                                                                            \
+        rgx[SLOT] = a_g; rmx[SLOT] = a_m; rsx[SLOT] = a_s; rsk[SLOT] = a_sk;         \
+        rkx[SLOT] = a_k; rmk[SLOT] = a_mk; rky[SLOT] = a_ky;                         \
+        cp[SLOT] = buf_[(ty + L) * PG_CC + tx];                                      \
+        ckx[SLOT] = buf_[FS + (ty + L) * PG_CC + tx];                                \
+        cky[SLOT] = buf_[2 * FS + (ty + L) * PG_CC + tx];                            \
+        if (k_ + S - 1 < nsteps) issue_row(ya - L + k_ + S - 1, (k_ + S - 1) % S);   \
+        cp_async_commit();                                                           \
     }
 
-    int step = 0;
-    // prologue: rows ya-L .. ya+L-1 (ya is a multiple of T)
 #pragma unroll
-    for (int k = 0; k < 2 * L; ++k) {
-        load_row(ya - L + k, step & 1);
-        __syncthreads();
-        PG_XPASS(step & 1, (k - L + T) % T);
-        ++step;
+    for (int k = 0; k < S - 1; ++k) {
+        if (k < nsteps) issue_row(ya - L + k, k);
+        cp_async_commit();
     }
+    // prologue: lead rows ya-L .. ya+L-1 (ya is a multiple of T)
+#pragma unroll
+    for (int k = 0; k < 2 * L; ++k) PG_STEP(k, (k - L + T) % T);
 
+    const Real beta = a.beta, hx = a.hx, hy = a.hy;
+    const Real strm = a.strm ? a.strm[n] : Real(0);
     double l1 = 0.0;
-    for (int y0 = ya; y0 < yb; y0 += T) {
+    int kbase = 2 * L;
+    for (int y0 = ya; y0 < yb; y0 += T, kbase += T) {
 #pragma unroll
         for (int s = 0; s < T; ++s) {
             const int y = y0 + s;
-            load_row(y + L, step & 1);
-            __syncthreads();
-            PG_XPASS(step & 1, (s + L) % T);
-            ++step;
+            PG_STEP(kbase + s, (s + L) % T);
             if (y < yb && xval && cval) {
                 Real px = 0, py = 0, kxp = 0, kxkp = 0, kxk = 0, kykp = 0, kyp = 0, kyk = 0;
 #pragma unroll
                 for (int b = 0; b < T; ++b) {
                     const int sl = (s - L + b + T) % T;
-                    px += a.t.m[b] * rgx[sl];
-                    py += a.t.gy[b] * rmx[sl];
-                    kxp += a.t.m[b] * rsx[sl];
-                    kxkp += a.t.m[b] * rsk[sl];
-                    kxk += a.t.m[b] * rkx[sl];
-                    kykp += a.t.sy[b] * rmk[sl];
-                    kyp += a.t.sy[b] * rmx[sl];
-                    kyk += a.t.sy[b] * rky[sl];
+                    px += Real(TP::m(b)) * rgx[sl];
+                    py += Real(TP::g(b)) * rmx[sl];
+                    kxp += Real(TP::m(b)) * rsx[sl];
+                    kxkp += Real(TP::m(b)) * rsk[sl];
+                    kxk += Real(TP::m(b)) * rkx[sl];
+                    kykp += Real(TP::s(b)) * rmk[sl];
+                    kyp += Real(TP::s(b)) * rmx[sl];
+                    kyk += Real(TP::s(b)) * rky[sl];
                 }
                 const Real pc = cp[s], kxc = ckx[s], kyc = cky[s];
-                const Real diffx = Real(0.5) * ((kxkp + kxc * kxp) - pc * kxk);
-                const Real diffy = Real(0.5) * ((kykp + kyc * kyp) - pc * kyk);
+                const Real diffx = hx * ((kxkp + kxc * kxp) - pc * kxk);
+                const Real diffy = hy * ((kykp + kyc * kyp) - pc * kyk);
                 const int64_t cell = (int64_t)x * g.ny + y;
                 const Real sig = a.sigma[cell * g.ng + gg];
                 const Real qq = a.q_per_dof ? a.q[cell * g.C + c] : a.q[cell * g.ng + gg];
-                const Real r = (((mu * px + nu * py) + diffx) + diffy) + sig * pc - qq;
+                const Real r = (((mu_dx * px + nu_dy * py) + diffx) + diffy) + sig * pc - qq;
                 if (SWEEP) {
-                    const Real d = a.beta * (a.strm[n] + sig);
-                    a.out[fidx(x, y, c, g.ny, a.out_h, g.C)] = pc - r / d;
+                    const Real d = beta * (strm + sig);
+                    a.out[fidx(x, y, c, g.ny, a.out_h, g.C)] = pc - fast_div(r, d);
                 } else {
                     if (a.r) a.r[fidx(x, y, c, g.ny, a.r_h, g.C)] = r;
                     l1 += fabs((double)r);
@@ -174,7 +233,8 @@ pg_residual_kernel(const PGResidArgs<Real, L> a) {
             }
         }
     }
-#undef PG_XPASS
+#undef PG_STEP
+    cp_async_wait<0>();
     if (!SWEEP && a.partials) {
         const double tot = block_sum(l1, red);
         if (threadIdx.x == 0 && threadIdx.y == 0)
@@ -185,35 +245,49 @@ pg_residual_kernel(const PGResidArgs<Real, L> a) {
 // ---------------------------------------------------------------------------------
 // K2: iterate averaging (R/multigrid.py:217-225) fused with the anisotropic
 // diffusivities (R/discretisation.py:114-161):
-//   psi_x = M_y G_x pbar,  psi_y = G_y M_x pbar             (stage 1, +-2l band)
-//   R_x = alpha_r mu (M_y M_x psi_x - psi_x)                  (stage 2, +-l band)
+//   psi_x = M_y G_x pbar / dx,  psi_y = G_y M_x pbar / dy       (stage 1, +-2l band)
+//   R_x = alpha_r mu (M_y M_x psi_x - psi_x)                      (stage 2, +-l band)
 //   k_x = min(dx|mu|, min(a_abs |R_x| dx/(eps+|psi_x|), a_sq R_x^2 dx/(eps+|mu| psi_x^2)))
 //   NaN / inf -> 0.   (y symmetric)
-// Outputs cover the band x, y in [-l, n+l).  Stage 1 runs on K_TXS x cells, stage 2
-// on the inner K_TXS - 2l (its x pass reads stage-1 neighbours through smem).
+// Outputs cover the band x, y in [-l, n+l).  Stage 1 runs on KTile x cells, stage 2
+// on the inner KTile - 2l (its x pass reads stage-1 neighbours through smem).
+// The averaged iterate pbar = (1 - theta) pbar_old + theta psi is formed on load
+// (both rows staged by cp.async) and written back for the cells this CTA owns.
 // ---------------------------------------------------------------------------------
-template <class Real, int L>
+template <class Real>
 struct PGKArgs {
     Geo g;
-    PGTaps<Real, L> t;
     const Real* psi; int psi_h;
     const Real* avg_in; int avg_in_h;
     Real* avg_out; int avg_out_h;
     int avg_mode; Real theta, omt;
-    Real alpha_r, eps, a_abs, a_sq, dx, dy;
+    Real alpha_r, eps, a_abs, a_sq, dx, dy, inv_dx, inv_dy;
     const Real* mu; const Real* nu;
     Real* kx; Real* ky; int k_h;
     int ly;     // output rows per CTA chunk (band coordinates), multiple of T
 };
 
 template <class Real, int L>
-__global__ void __launch_bounds__(PG_CC * K_TXS)
-pg_diffusivity_kernel(const PGKArgs<Real, L> a) {
+constexpr size_t pg_k_smem() {
+    constexpr int KT = KTile<Real, L>::value;
+    return ((size_t)PGStages<Real>::value * 2 * (KT + 2 * L) * PG_CC +
+            (size_t)2 * 2 * KT * PG_CC) * sizeof(Real);
+}
+
+template <class Real, int L>
+__global__ void __launch_bounds__(PG_CC * KTile<Real, L>::value)
+pg_diffusivity_kernel(const PGKArgs<Real> a) {
+    using TP = UnitTaps<L>;
+    constexpr int KT = KTile<Real, L>::value;
     constexpr int T = 2 * L + 1;
-    constexpr int TXO = K_TXS - 2 * L;
-    constexpr int W1 = K_TXS + 2 * L;
-    __shared__ Real s1[2][W1][PG_CC];
-    __shared__ Real s2[2][2][K_TXS][PG_CC];
+    constexpr int TXO = KT - 2 * L;
+    constexpr int W1 = KT + 2 * L;
+    constexpr int NX = (W1 + KT - 1) / KT;
+    constexpr int S = PGStages<Real>::value;
+    constexpr int FS = W1 * PG_CC;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    Real* s1 = reinterpret_cast<Real*>(smraw);          // [S][2][W1][CC]: pbar/psi, pbar_old
+    Real* s2 = s1 + (size_t)S * 2 * FS;                  // [2][2][KT][CC]: psi_x, psi_y
 
     const Geo& g = a.g;
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -227,85 +301,127 @@ pg_diffusivity_kernel(const PGKArgs<Real, L> a) {
     const int x0o = -L + (int)blockIdx.x * TXO;   // first output x of this CTA
     const int x0s = x0o - L;                       // first stage-1 x
     const int xs = x0s + ty;
-    const bool s2thr = ty >= L && ty < K_TXS - L;
+    const bool s2thr = ty >= L && ty < KT - L;
     const bool xout = s2thr && xs < g.nx + L;
     const int ua = blockIdx.z * a.ly;                      // band rows u = y + L
     const int ub = min(g.ny + 2 * L, ua + a.ly);
-    // psi_avg rows / columns this CTA owns (each interior cell written once)
     const int ox0 = max(x0o, 0), ox1 = min(x0o + TXO, g.nx);
     const int oy0 = max(ua - L, 0), oy1 = min(ub - L, g.ny);
     const Real ar_mu = a.alpha_r * mu, ar_nu = a.alpha_r * nu;
+    const Real dx = a.dx, dy = a.dy, inv_dx = a.inv_dx, inv_dy = a.inv_dy;
+    const Real kxmax = dx * amu, kymax = dy * anu;
+    const Real eps = a.eps, a_abs = a.a_abs, a_sq = a.a_sq;
+    const bool ema = a.avg_mode == 2;
+    const bool write_avg = a.avg_mode != 0 && cval;
+
+    constexpr int PRE = ((4 * L + T - 1) / T) * T;
+    const int vs = ua - PRE;
+    const int nsteps = PRE + (int)(((ub - ua) + T - 1) / T) * T;
+
+    const int64_t pp = (int64_t)(g.ny + 2 * a.psi_h) * g.C;
+    const int64_t ap = (int64_t)(g.ny + 2 * a.avg_in_h) * g.C;
+    const int64_t op = (int64_t)(g.ny + 2 * a.avg_out_h) * g.C;
+    int64_t pxo[NX], axo[NX], oxo[NX];
+    bool pz[NX], own[NX];
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+        const int xi = ty + j * KT;
+        int xg = x0s - L + xi, xr = xg;
+        bool zero = !cval || xi >= W1;
+        if (xr < 0) { if (!g.ghost_w) { zero |= mpos; xr = 0; } }
+        else if (xr >= g.nx) { if (!g.ghost_e) { zero |= !mpos; xr = g.nx - 1; } }
+        pz[j] = zero;
+        pxo[j] = (int64_t)(xr + a.psi_h) * pp + c;
+        axo[j] = (int64_t)(xr + a.avg_in_h) * ap + c;
+        own[j] = write_avg && xi < W1 && xg >= ox0 && xg < ox1;
+        oxo[j] = (int64_t)(xg + a.avg_out_h) * op + c;
+    }
+
+    auto issue_row = [&](int yy, int b) {     // pbar lead row y = yy into buffer b
+        Real* base = s1 + (size_t)b * 2 * FS;
+        bool yz = false;
+        int yr = yy;
+        if (yr < 0) { yz = npos; yr = 0; }
+        else if (yr >= g.ny) { yz = !npos; yr = g.ny - 1; }
+        const int64_t prow = (int64_t)(yr + a.psi_h) * g.C;
+        const int64_t arow = (int64_t)(yr + a.avg_in_h) * g.C;
+#pragma unroll
+        for (int j = 0; j < NX; ++j) {
+            const int xi = ty + j * KT;
+            if (xi < W1) {
+                const bool ok = !(pz[j] || yz);
+                cp_async<sizeof(Real)>(base + xi * PG_CC + tx, a.psi + (ok ? pxo[j] + prow : 0), ok);
+                if (ema)
+                    cp_async<sizeof(Real)>(base + FS + xi * PG_CC + tx,
+                                           a.avg_in + (ok ? axo[j] + arow : 0), ok);
+            }
+        }
+    };
 
     Real r1g[T], r1m[T];   // stage-1 x pass of pbar (by pbar row)
     Real c1x[T], c1y[T];   // psi_x, psi_y (by row)
     Real r2x[T], r2y[T];   // M_x psi_x, M_x psi_y (by row)
 
-    auto load_row = [&](int yy, int buf) {
-        for (int xi = ty; xi < W1; xi += K_TXS) {
-            const int xg = x0s - L + xi;
-            Real v = Real(0);
-            if (cval) {
-                int xr = xg, yr = yy;
-                if (resolve_vac(xr, yr, g, mpos, npos)) {
-                    const Real pv = a.psi[fidx(xr, yr, c, g.ny, a.psi_h, g.C)];
-                    if (a.avg_mode == 2) {
-                        const Real av = a.avg_in[fidx(xr, yr, c, g.ny, a.avg_in_h, g.C)];
-                        v = av * a.omt + a.theta * pv;
-                    } else {
-                        v = pv;
-                    }
-                    if (a.avg_mode != 0 && xr == xg && yr == yy && xg >= ox0 && xg < ox1 &&
-                        yy >= oy0 && yy < oy1)
-                        a.avg_out[fidx(xg, yy, c, g.ny, a.avg_out_h, g.C)] = v;
-                }
-            }
-            s1[buf][xi][tx] = v;
-        }
-    };
-
-    // steps v (band row of the stage-2 output) from vs to ve, vs = ua - T*ceil(4L/T)
-    constexpr int PRE = ((4 * L + T - 1) / T) * T;
-    const int vs = ua - PRE;
+#pragma unroll
+    for (int k = 0; k < S - 1; ++k) {
+        if (k < nsteps) issue_row(vs + L + k, k);
+        cp_async_commit();
+    }
     int step = 0;
     for (int v0 = vs; v0 < ub; v0 += T) {
 #pragma unroll
         for (int s = 0; s < T; ++s) {
             const int v = v0 + s;
-            const int buf = step & 1;
-            ++step;
-            // (1) pbar lead row: band row v + 2L  <=>  y = v + L
-            load_row(v + L, buf);
+            const int yl = v + L;                  // pbar lead row (y coords)
+            cp_async_wait<S - 2>();
+            Real* buf = s1 + (size_t)(step % S) * 2 * FS;
+            const bool own_row = yl >= oy0 && yl < oy1;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) {         // form pbar on own elements
+                const int xi = ty + j * KT;
+                if (xi < W1) {
+                    Real pv = buf[xi * PG_CC + tx];
+                    if (ema) pv = buf[FS + xi * PG_CC + tx] * a.omt + a.theta * pv;
+                    buf[xi * PG_CC + tx] = pv;
+                    if (own[j] && own_row) a.avg_out[oxo[j] + (int64_t)(yl + a.avg_out_h) * g.C] = pv;
+                }
+            }
             __syncthreads();
-            // (2) stage 1 at band row v + L (y = v): x pass of the lead row, then y pass
-            {
+            Real* s2b = s2 + (size_t)(step & 1) * 2 * KT * PG_CC;
+            {   // stage 1 at band row v + L (y = v)
                 Real ag = 0, am = 0;
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
-                    const Real p = s1[buf][ty + t][tx];
-                    ag += a.t.gx[t] * p;
-                    am += a.t.m[t] * p;
+                    const Real p = buf[(ty + t) * PG_CC + tx];
+                    ag += Real(TP::g(t)) * p;
+                    am += Real(TP::m(t)) * p;
                 }
                 r1g[(s + 2 * L) % T] = ag;
                 r1m[(s + 2 * L) % T] = am;
                 Real px = 0, py = 0;
 #pragma unroll
                 for (int b = 0; b < T; ++b) {
-                    px += a.t.m[b] * r1g[(s + b) % T];
-                    py += a.t.gy[b] * r1m[(s + b) % T];
+                    px += Real(TP::m(b)) * r1g[(s + b) % T];
+                    py += Real(TP::g(b)) * r1m[(s + b) % T];
                 }
+                px *= inv_dx;
+                py *= inv_dy;
                 c1x[(s + L) % T] = px;
                 c1y[(s + L) % T] = py;
-                s2[buf][0][ty][tx] = px;
-                s2[buf][1][ty][tx] = py;
+                s2b[ty * PG_CC + tx] = px;
+                s2b[(KT + ty) * PG_CC + tx] = py;
             }
+            if (step + S - 1 < nsteps) issue_row(vs + L + step + S - 1, (step + S - 1) % S);
+            cp_async_commit();
+            ++step;
             __syncthreads();
-            // (3) stage 2: x pass (mass) at band row v + L, y pass (mass) -> row v
+            // stage 2: x pass (mass) at band row v + L, y pass (mass) -> row v
             if (s2thr) {
                 Real mx = 0, my = 0;
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
-                    mx += a.t.m[t] * s2[buf][0][ty - L + t][tx];
-                    my += a.t.m[t] * s2[buf][1][ty - L + t][tx];
+                    mx += Real(TP::m(t)) * s2b[(ty - L + t) * PG_CC + tx];
+                    my += Real(TP::m(t)) * s2b[(KT + ty - L + t) * PG_CC + tx];
                 }
                 r2x[(s + L) % T] = mx;
                 r2y[(s + L) % T] = my;
@@ -313,28 +429,28 @@ pg_diffusivity_kernel(const PGKArgs<Real, L> a) {
                     Real mmx = 0, mmy = 0;
 #pragma unroll
                     for (int b = 0; b < T; ++b) {
-                        mmx += a.t.m[b] * r2x[(s - L + b + T) % T];
-                        mmy += a.t.m[b] * r2y[(s - L + b + T) % T];
+                        mmx += Real(TP::m(b)) * r2x[(s - L + b + T) % T];
+                        mmy += Real(TP::m(b)) * r2y[(s - L + b + T) % T];
                     }
                     const Real px = c1x[s % T], py = c1y[s % T];
                     const Real rx = ar_mu * (mmx - px);
                     const Real ry = ar_nu * (mmy - py);
-                    Real kx = nanmin(a.dx * amu,
-                                     nanmin(a.a_abs * fabs(rx) * a.dx / (a.eps + fabs(px)),
-                                            a.a_sq * (rx * rx) * a.dx / (a.eps + amu * (px * px))));
-                    Real ky = nanmin(a.dy * anu,
-                                     nanmin(a.a_abs * fabs(ry) * a.dy / (a.eps + fabs(py)),
-                                            a.a_sq * (ry * ry) * a.dy / (a.eps + anu * (py * py))));
+                    Real kx = nanmin(kxmax,
+                                     nanmin(fast_div(a_abs * fabs(rx) * dx, eps + fabs(px)),
+                                            fast_div(a_sq * (rx * rx) * dx, eps + amu * (px * px))));
+                    Real ky = nanmin(kymax,
+                                     nanmin(fast_div(a_abs * fabs(ry) * dy, eps + fabs(py)),
+                                            fast_div(a_sq * (ry * ry) * dy, eps + anu * (py * py))));
                     if (!isfinite(kx)) kx = Real(0);
                     if (!isfinite(ky)) ky = Real(0);
-                    const int yo = v - L;
-                    const int64_t o = fidx(xs, yo, c, g.ny, a.k_h, g.C);
+                    const int64_t o = fidx(xs, v - L, c, g.ny, a.k_h, g.C);
                     a.kx[o] = kx;
                     a.ky[o] = ky;
                 }
             }
         }
     }
+    cp_async_wait<0>();
 }
 
 }  // namespace csn
