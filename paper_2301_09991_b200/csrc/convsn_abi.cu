@@ -164,19 +164,23 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
     }
     a.sigma = (const Real*)sigma; a.mu = (const Real*)mu; a.nu = (const Real*)nu;
     a.strm = (const Real*)strm;
-    a.dx = (Real)g->dx; a.dy = (Real)g->dy;
+    a.inv_dx = (Real)(1.0 / g->dx); a.inv_dy = (Real)(1.0 / g->dy);
     a.scale = (Real)diag_scale; a.use_scale = diag_scale != 1.0;
     a.out = (Real*)out; a.out_h = out_h;
-    a.n_sweeps = n_sweeps;
-    const int gx = (int)cdiv(g->nx, UP_XW - 2 * n_sweeps);
+    const int gx = (int)cdiv(cdiv(g->ny, UT), UP_SPB);
     const int gy = (int)cdiv((int64_t)g->nd * g->ng, UP_CC);
-    // y chunks: enough CTAs to fill the machine, chunks long against the 2H warm-up
-    int chunks = 1;
-    while ((int64_t)gx * gy * chunks < 148 * 4 && g->ny / (chunks * 2) >= 8 * (n_sweeps + 1))
-        chunks *= 2;
-    a.ly = (int)cdiv(g->ny, chunks);
-    const int gz = (int)cdiv(g->ny, a.ly);
-    upwind_smooth_kernel<Real><<<dim3(gx, gy, gz), dim3(UP_CC, UP_XW), 0, st>>>(a);
+    // x chunks: keep chunks long against the H-column warm-up, fill the machine
+    int chunks = (int)cdiv(g->nx, UP_XCHUNK);
+    while (chunks > 1 && (int64_t)gx * gy * (chunks / 2) >= 148 * 8) chunks /= 2;
+    a.xchunk = (int)cdiv(g->nx, chunks);
+    const int gz = (int)cdiv(g->nx, a.xchunk);
+    dim3 grid(gx, gy, gz), block(UP_CC, UP_SPB);
+    switch (n_sweeps) {
+        case 0: upwind_smooth_kernel<Real, 0><<<grid, block, 0, st>>>(a); break;
+        case 1: upwind_smooth_kernel<Real, 1><<<grid, block, 0, st>>>(a); break;
+        case 2: upwind_smooth_kernel<Real, 2><<<grid, block, 0, st>>>(a); break;
+        default: upwind_smooth_kernel<Real, 3><<<grid, block, 0, st>>>(a); break;
+    }
     CSN_CHECK_LAUNCH();
     return CSN_OK;
 }
