@@ -57,6 +57,111 @@ __device__ __forceinline__ void cp_async(void* smem, const void* gmem, bool vali
                  "n"(BYTES), "r"(n)
                  : "memory");
 }
+// same with an already converted 32-bit shared-space address
+template <int BYTES>
+__device__ __forceinline__ void cp_async_s(unsigned saddr, const void* gmem, bool valid) {
+    const int n = valid ? BYTES : 0;
+    if (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem),
+                     "r"(n)
+                     : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(saddr), "l"(gmem),
+                     "n"(BYTES), "r"(n)
+                     : "memory");
+}
+
+// Row stager of the y-marching stencil kernels.  A staged row holds up to 4 fields x
+// W cells x 32 channels (smem layout [field][cell][channel]).  An item is one
+// (cell, VEC-channel group) and stages that vector of every field, so the thread
+// that owns an item can post-process it (psi - delta, the EMA) right after its own
+// copies land.  Everything row independent — shared address, x resolution of the
+// vacuum rule, x part of the global offset — is computed once; per row only the y
+// rule and one multiply-add per field remain.
+//   kind 0 field (psi-like): vacuum rule (zero on incoming sides, else clamp);
+//   kind 1 field (k-like):   stored on the +-L band, zero outside it, never clamped.
+struct FieldDesc {
+    const void* ptr;   // nullptr: field reads as 0
+    int halo;
+    int kind;
+};
+
+template <class Real, int VEC, int NI, int NF>
+struct Stager {
+    unsigned soff[NI];          // shared byte offset of the item (field 0, buffer 0)
+    int64_t xoff[NI][NF];       // element offset of (x storage, y storage 0, channel)
+    bool xz[NI][NF];            // zero because of x (or invalid channel / no item)
+    bool npos[NI];
+    bool item[NI];              // this thread has an item in slot i
+    int ny, C, band;
+    int halo[NF];
+    int kind[NF];
+    const Real* ptr[NF];
+
+    // x0: global x of staged cell 0; W cells; c0: first channel of the CTA
+    __device__ __forceinline__ void init(const Geo& g, const FieldDesc* fd, int x0, int W,
+                                         int c0, int band_, const Real* mu, const Real* nu,
+                                         int tid, int nthreads) {
+        constexpr int G4 = 32 / VEC;
+        ny = g.ny; C = g.C; band = band_;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            ptr[f] = (const Real*)fd[f].ptr;
+            halo[f] = fd[f].halo;
+            kind[f] = fd[f].kind;
+        }
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int e = tid + i * nthreads;
+            const bool has = e < W * G4;
+            item[i] = has;
+            const int xi = has ? e / G4 : 0, q = has ? e % G4 : 0;
+            const int c = c0 + q * VEC;
+            const bool cval = has && c < g.C;
+            const int n = (cval ? c : 0) / g.ng;
+            const bool mp = mu[n] > Real(0);
+            npos[i] = nu[n] > Real(0);
+            soff[i] = (unsigned)((xi * 32 + q * VEC) * sizeof(Real));
+            const int xg = x0 + xi;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                bool z = !cval || fd[f].ptr == nullptr;
+                int xr = xg;
+                if (fd[f].kind == 0) {
+                    if (xr < 0) { if (!g.ghost_w) { z |= mp; xr = 0; } }
+                    else if (xr >= g.nx) { if (!g.ghost_e) { z |= !mp; xr = g.nx - 1; } }
+                } else {
+                    z |= xg < -band || xg >= g.nx + band;
+                }
+                xz[i][f] = z;
+                xoff[i][f] = (int64_t)(xr + fd[f].halo) * (int64_t)(g.ny + 2 * fd[f].halo) * g.C + c;
+            }
+        }
+    }
+
+    // stage row yy into the buffer at shared address sbuf (field stride fstride bytes)
+    __device__ __forceinline__ void issue(int yy, unsigned sbuf, unsigned fstride) const {
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            if (!item[i]) continue;
+            bool yz0 = false;
+            int yr = yy;
+            if (yr < 0) { yz0 = npos[i]; yr = 0; }
+            else if (yr >= ny) { yz0 = !npos[i]; yr = ny - 1; }
+            const bool yz1 = yy < -band || yy >= ny + band;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                const bool z = xz[i][f] || (kind[f] == 0 ? yz0 : yz1);
+                const int ys = (kind[f] == 0 ? yr : yy) + halo[f];
+                const Real* src = z ? ptr[0] : ptr[f] + xoff[i][f] + (int64_t)ys * C;
+                cp_async_s<VEC * (int)sizeof(Real)>(sbuf + f * fstride + soff[i], src, !z);
+            }
+        }
+    }
+};
+
+}  // namespace csn
+namespace csn {
 __device__ __forceinline__ void cp_async_commit() {
     asm volatile("cp.async.commit_group;\n" ::: "memory");
 }

@@ -58,6 +58,30 @@ void set_smem(K kernel, size_t bytes) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+// 16-byte staging needs every aligned VEC-channel group inside one octahedron face
+// (same upwind signs) and VEC | C (alignment): a face holds n_a^2 * ng channels.
+inline bool vec_ok(const csn_geom* g, int vec) {
+    const int64_t C = (int64_t)g->nd * g->ng;
+    const int64_t face = (int64_t)g->na * g->na * g->ng;
+    return C % vec == 0 && face % vec == 0 && 8 * face == C;
+}
+
+template <class Real, int L, bool SWEEP, int VEC>
+void launch_pg_resid(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<Real>& a) {
+    constexpr size_t sm = pg_residual_smem<Real, L, SWEEP>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_residual_kernel<Real, L, SWEEP, VEC>, sm); attr = true; }
+    pg_residual_kernel<Real, L, SWEEP, VEC><<<grid, block, sm, st>>>(a);
+}
+
+template <class Real, int L, bool EMA, int VEC>
+void launch_pg_k(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<Real>& a) {
+    constexpr size_t sm = pg_k_smem<Real, L, EMA>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_diffusivity_kernel<Real, L, EMA, VEC>, sm); attr = true; }
+    pg_diffusivity_kernel<Real, L, EMA, VEC><<<grid, block, sm, st>>>(a);
+}
+
 // ------------------------------------------------------------------ PG residual
 template <class Real, int L>
 int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int psi_h,
@@ -85,18 +109,15 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
     const int gz = (int)cdiv(g->ny, a.ly);
     a.partials = (l1 || partials) ? partials : nullptr;
     dim3 grid(gx, gy, gz), block(PG_CC, PG_TX);
+    const bool vec = vec_ok(g, 16 / (int)sizeof(Real));
     if (out) {
-        constexpr size_t sm = pg_residual_smem<Real, L, true>();
-        static bool attr = false;
-        if (!attr) { set_smem(pg_residual_kernel<Real, L, true>, sm); attr = true; }
-        pg_residual_kernel<Real, L, true><<<grid, block, sm, st>>>(a);
+        if (vec) launch_pg_resid<Real, L, true, 16 / sizeof(Real)>(grid, block, st, a);
+        else launch_pg_resid<Real, L, true, 1>(grid, block, st, a);
         CSN_CHECK_LAUNCH();
     } else {
         if (l1 && !partials) return CSN_E_ARG;
-        constexpr size_t sm = pg_residual_smem<Real, L, false>();
-        static bool attr = false;
-        if (!attr) { set_smem(pg_residual_kernel<Real, L, false>, sm); attr = true; }
-        pg_residual_kernel<Real, L, false><<<grid, block, sm, st>>>(a);
+        if (vec) launch_pg_resid<Real, L, false, 16 / sizeof(Real)>(grid, block, st, a);
+        else launch_pg_resid<Real, L, false, 1>(grid, block, st, a);
         CSN_CHECK_LAUNCH();
         if (l1) {
             sum_f64_kernel<<<1, 1024, 0, st>>>(partials, (int64_t)gx * gy * gz, 1.0, l1);
@@ -135,10 +156,15 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
     a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T);
     const int gz = (int)cdiv(g->ny + 2 * L, a.ly);
     dim3 grid(gx, gy, gz), block(PG_CC, KT);
-    constexpr size_t sm = pg_k_smem<Real, L>();
-    static bool attr = false;
-    if (!attr) { set_smem(pg_diffusivity_kernel<Real, L>, sm); attr = true; }
-    pg_diffusivity_kernel<Real, L><<<grid, block, sm, st>>>(a);
+    constexpr int V = 16 / sizeof(Real);
+    const bool vec = vec_ok(g, V);
+    if (avg_mode == 2) {
+        if (vec) launch_pg_k<Real, L, true, V>(grid, block, st, a);
+        else launch_pg_k<Real, L, true, 1>(grid, block, st, a);
+    } else {
+        if (vec) launch_pg_k<Real, L, false, V>(grid, block, st, a);
+        else launch_pg_k<Real, L, false, 1>(grid, block, st, a);
+    }
     CSN_CHECK_LAUNCH();
     return CSN_OK;
 }

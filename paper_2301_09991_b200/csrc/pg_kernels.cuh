@@ -67,13 +67,14 @@ constexpr size_t pg_residual_smem() {
     return (size_t)PGStages<Real>::value * (SWEEP ? 4 : 3) * (PG_TX + 2 * L) * PG_CC * sizeof(Real);
 }
 
-template <class Real, int L, bool SWEEP>
+template <class Real, int L, bool SWEEP, int VEC>
 __global__ void __launch_bounds__(PG_CC * PG_TX, (sizeof(Real) == 4 && L <= 3) ? 2 : 1)
 pg_residual_kernel(const PGResidArgs<Real> a) {
     using TP = UnitTaps<L>;
     constexpr int T = 2 * L + 1;
     constexpr int W = PG_TX + 2 * L;
-    constexpr int NX = (W + PG_TX - 1) / PG_TX;    // staged cells per thread
+    constexpr int NT = PG_CC * PG_TX;
+    constexpr int NI = (W * (PG_CC / VEC) + NT - 1) / NT;   // staged items per thread
     constexpr int NF = SWEEP ? 4 : 3;              // psi, kx, ky (, delta)
     constexpr int S = PGStages<Real>::value;       // rows in flight
     constexpr int FS = W * PG_CC;                  // elements per field row
@@ -83,12 +84,13 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
 
     const Geo& g = a.g;
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const int c = blockIdx.y * PG_CC + tx;
+    const int tid = ty * PG_CC + tx;
+    const int c0 = blockIdx.y * PG_CC;
+    const int c = c0 + tx;
     const bool cval = c < g.C;
     const int cs = cval ? c : g.C - 1;
     const int n = cs / g.ng, gg = cs - n * g.ng;
     const Real mu = a.mu[n], nu = a.nu[n];
-    const bool mpos = mu > Real(0), npos = nu > Real(0);
     const Real mu_dx = mu * a.inv_dx, nu_dy = nu * a.inv_dy;
     const int x0 = blockIdx.x * PG_TX;
     const int x = x0 + ty;
@@ -97,54 +99,12 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
     const bool xval = x < g.nx;
     const int nsteps = 2 * L + (int)(((yb - ya) + T - 1) / T) * T;   // lead rows ya-L ...
 
-    // row-independent part of the staging addresses of this thread's cells
-    const int64_t pp = (int64_t)(g.ny + 2 * a.psi_h) * g.C;        // psi x pitch
-    const int64_t dp = (int64_t)(g.ny + 2 * a.delta_h) * g.C;
-    const int64_t kp = (int64_t)(g.ny + 2 * a.k_h) * g.C;
-    int64_t pxo[NX], dxo[NX], kxo[NX];
-    bool pz[NX], kz[NX];
-#pragma unroll
-    for (int j = 0; j < NX; ++j) {
-        const int xi = ty + j * PG_TX;
-        int xg = x0 - L + xi, xr = xg;
-        bool zero = !cval || xi >= W;
-        if (xr < 0) { if (!g.ghost_w) { zero |= mpos; xr = 0; } }
-        else if (xr >= g.nx) { if (!g.ghost_e) { zero |= !mpos; xr = g.nx - 1; } }
-        pz[j] = zero;
-        pxo[j] = (int64_t)(xr + a.psi_h) * pp + c;
-        dxo[j] = (int64_t)(xr + a.delta_h) * dp + c;
-        kz[j] = !cval || xi >= W || xg < -L || xg >= g.nx + L;
-        kxo[j] = (int64_t)(xg + a.k_h) * kp + c;
-    }
-
-    auto issue_row = [&](int yy, int b) {
-        Real* base = sm + (size_t)b * NF * FS;
-        bool yz = false;
-        int yr = yy;
-        if (yr < 0) { yz = npos; yr = 0; }
-        else if (yr >= g.ny) { yz = !npos; yr = g.ny - 1; }
-        const bool kyz = yy < -L || yy >= g.ny + L;
-        const int64_t prow = (int64_t)(yr + a.psi_h) * g.C;
-        const int64_t drow = (int64_t)(yr + a.delta_h) * g.C;
-        const int64_t krow = (int64_t)(yy + a.k_h) * g.C;
-#pragma unroll
-        for (int j = 0; j < NX; ++j) {
-            const int xi = ty + j * PG_TX;
-            if (xi < W) {
-                Real* dst = base + xi * PG_CC + tx;
-                const bool ok = !(pz[j] || yz);
-                cp_async<sizeof(Real)>(dst, a.psi + (ok ? pxo[j] + prow : 0), ok);
-                if (SWEEP) {
-                    const bool okd = ok && a.delta != nullptr;
-                    cp_async<sizeof(Real)>(dst + 3 * FS, okd ? a.delta + dxo[j] + drow : a.psi, okd);
-                }
-                const bool kok = !(kz[j] || kyz);
-                const int64_t ko = kok ? kxo[j] + krow : 0;
-                cp_async<sizeof(Real)>(dst + FS, a.kx + ko, kok);
-                cp_async<sizeof(Real)>(dst + 2 * FS, a.ky + ko, kok);
-            }
-        }
-    };
+    FieldDesc fd[4] = {{a.psi, a.psi_h, 0}, {a.kx, a.k_h, 1}, {a.ky, a.k_h, 1},
+                       {a.delta, a.delta_h, 0}};
+    Stager<Real, VEC, NI, NF> st;
+    st.init(g, fd, x0 - L, W, c0, L, a.mu, a.nu, tid, NT);
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(sm);
+    constexpr unsigned FSB = FS * sizeof(Real);
 
     // x-pass rings (by row mod T), unit taps
     Real rgx[T], rmx[T], rsx[T], rsk[T], rkx[T], rmk[T], rky[T];
@@ -156,9 +116,12 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
         cp_async_wait<S - 2>();                                                      \
         Real* buf_ = sm + (size_t)(k_ % S) * NF * FS;                                \
         if (SWEEP) {                                                                 \
-            _Pragma("unroll") for (int j = 0; j < NX; ++j) {                         \
-                const int xi = ty + j * PG_TX;                                       \
-                if (xi < W) buf_[xi * PG_CC + tx] -= buf_[3 * FS + xi * PG_CC + tx]; \
+            _Pragma("unroll") for (int i = 0; i < NI; ++i) {                         \
+                const int e = tid + i * NT;                                          \
+                if (e < W * (PG_CC / VEC)) {                                         \
+                    Real* p_ = buf_ + (e / (PG_CC / VEC)) * PG_CC + (e % (PG_CC / VEC)) * VEC; \
+                    _Pragma("unroll") for (int v = 0; v < VEC; ++v) p_[v] -= p_[3 * FS + v]; \
+                }                                                                    \
             }                                                                        \
         }                                                                            \
         __syncthreads();                                                             \
@@ -180,13 +143,14 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
         cp[SLOT] = buf_[(ty + L) * PG_CC + tx];                                      \
         ckx[SLOT] = buf_[FS + (ty + L) * PG_CC + tx];                                \
         cky[SLOT] = buf_[2 * FS + (ty + L) * PG_CC + tx];                            \
-        if (k_ + S - 1 < nsteps) issue_row(ya - L + k_ + S - 1, (k_ + S - 1) % S);   \
+        if (k_ + S - 1 < nsteps)                                                     \
+            st.issue(ya - L + k_ + S - 1, sbase + ((k_ + S - 1) % S) * NF * FSB, FSB); \
         cp_async_commit();                                                           \
     }
 
 #pragma unroll
     for (int k = 0; k < S - 1; ++k) {
-        if (k < nsteps) issue_row(ya - L + k, k);
+        if (k < nsteps) st.issue(ya - L + k, sbase + k * NF * FSB, FSB);
         cp_async_commit();
     }
     // prologue: lead rows ya-L .. ya+L-1 (ya is a multiple of T)
@@ -195,6 +159,7 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
 
     const Real beta = a.beta, hx = a.hx, hy = a.hy;
     const Real strm = a.strm ? a.strm[n] : Real(0);
+    const int64_t cell0 = (int64_t)(xval ? x : 0) * g.ny;
     double l1 = 0.0;
     int kbase = 2 * L;
     for (int y0 = ya; y0 < yb; y0 += T, kbase += T) {
@@ -219,7 +184,7 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
                 const Real pc = cp[s], kxc = ckx[s], kyc = cky[s];
                 const Real diffx = hx * ((kxkp + kxc * kxp) - pc * kxk);
                 const Real diffy = hy * ((kykp + kyc * kyp) - pc * kyk);
-                const int64_t cell = (int64_t)x * g.ny + y;
+                const int64_t cell = cell0 + y;
                 const Real sig = a.sigma[cell * g.ng + gg];
                 const Real qq = a.q_per_dof ? a.q[cell * g.C + c] : a.q[cell * g.ng + gg];
                 const Real r = (((mu_dx * px + nu_dy * py) + diffx) + diffy) + sig * pc - qq;
@@ -267,14 +232,14 @@ struct PGKArgs {
     int ly;     // output rows per CTA chunk (band coordinates), multiple of T
 };
 
-template <class Real, int L>
+template <class Real, int L, bool EMA>
 constexpr size_t pg_k_smem() {
     constexpr int KT = KTile<Real, L>::value;
-    return ((size_t)PGStages<Real>::value * 2 * (KT + 2 * L) * PG_CC +
+    return ((size_t)PGStages<Real>::value * (EMA ? 2 : 1) * (KT + 2 * L) * PG_CC +
             (size_t)2 * 2 * KT * PG_CC) * sizeof(Real);
 }
 
-template <class Real, int L>
+template <class Real, int L, bool EMA, int VEC>
 __global__ void __launch_bounds__(PG_CC * KTile<Real, L>::value)
 pg_diffusivity_kernel(const PGKArgs<Real> a) {
     using TP = UnitTaps<L>;
@@ -282,27 +247,31 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
     constexpr int T = 2 * L + 1;
     constexpr int TXO = KT - 2 * L;
     constexpr int W1 = KT + 2 * L;
-    constexpr int NX = (W1 + KT - 1) / KT;
+    constexpr int NT = PG_CC * KT;
+    constexpr int G4 = PG_CC / VEC;
+    constexpr int NI = (W1 * G4 + NT - 1) / NT;
+    constexpr int NF = EMA ? 2 : 1;               // psi (, pbar_old)
     constexpr int S = PGStages<Real>::value;
     constexpr int FS = W1 * PG_CC;
     extern __shared__ __align__(16) unsigned char smraw[];
-    Real* s1 = reinterpret_cast<Real*>(smraw);          // [S][2][W1][CC]: pbar/psi, pbar_old
-    Real* s2 = s1 + (size_t)S * 2 * FS;                  // [2][2][KT][CC]: psi_x, psi_y
+    Real* s1 = reinterpret_cast<Real*>(smraw);          // [S][NF][W1][CC]
+    Real* s2 = s1 + (size_t)S * NF * FS;                 // [2][2][KT][CC]: psi_x, psi_y
 
     const Geo& g = a.g;
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const int c = blockIdx.y * PG_CC + tx;
+    const int tid = ty * PG_CC + tx;
+    const int c0 = blockIdx.y * PG_CC;
+    const int c = c0 + tx;
     const bool cval = c < g.C;
     const int cs = cval ? c : g.C - 1;
     const int n = cs / g.ng;
     const Real mu = a.mu[n], nu = a.nu[n];
     const Real amu = fabs(mu), anu = fabs(nu);
-    const bool mpos = mu > Real(0), npos = nu > Real(0);
     const int x0o = -L + (int)blockIdx.x * TXO;   // first output x of this CTA
     const int x0s = x0o - L;                       // first stage-1 x
     const int xs = x0s + ty;
     const bool s2thr = ty >= L && ty < KT - L;
-    const bool xout = s2thr && xs < g.nx + L;
+    const bool xout = s2thr && xs < g.nx + L && cval;
     const int ua = blockIdx.z * a.ly;                      // band rows u = y + L
     const int ub = min(g.ny + 2 * L, ua + a.ly);
     const int ox0 = max(x0o, 0), ox1 = min(x0o + TXO, g.nx);
@@ -310,53 +279,30 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
     const Real ar_mu = a.alpha_r * mu, ar_nu = a.alpha_r * nu;
     const Real dx = a.dx, dy = a.dy, inv_dx = a.inv_dx, inv_dy = a.inv_dy;
     const Real kxmax = dx * amu, kymax = dy * anu;
-    const Real eps = a.eps, a_abs = a.a_abs, a_sq = a.a_sq;
-    const bool ema = a.avg_mode == 2;
-    const bool write_avg = a.avg_mode != 0 && cval;
+    const Real eps = a.eps, cabs_x = a.a_abs * dx, csq_x = a.a_sq * dx;
+    const Real cabs_y = a.a_abs * dy, csq_y = a.a_sq * dy;
+    const Real omt = a.omt, theta = a.theta;
+    const bool write_avg = a.avg_mode != 0;
 
     constexpr int PRE = ((4 * L + T - 1) / T) * T;
     const int vs = ua - PRE;
     const int nsteps = PRE + (int)(((ub - ua) + T - 1) / T) * T;
 
-    const int64_t pp = (int64_t)(g.ny + 2 * a.psi_h) * g.C;
-    const int64_t ap = (int64_t)(g.ny + 2 * a.avg_in_h) * g.C;
-    const int64_t op = (int64_t)(g.ny + 2 * a.avg_out_h) * g.C;
-    int64_t pxo[NX], axo[NX], oxo[NX];
-    bool pz[NX], own[NX];
+    FieldDesc fd[2] = {{a.psi, a.psi_h, 0}, {a.avg_in, a.avg_in_h, 0}};
+    Stager<Real, VEC, NI, NF> st;
+    st.init(g, fd, x0s - L, W1, c0, 0, a.mu, a.nu, tid, NT);
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(s1);
+    constexpr unsigned FSB = FS * sizeof(Real);
+    // owned pbar write-back per item: output pointer at y storage 0, or null
+    Real* own_ptr[NI];
 #pragma unroll
-    for (int j = 0; j < NX; ++j) {
-        const int xi = ty + j * KT;
-        int xg = x0s - L + xi, xr = xg;
-        bool zero = !cval || xi >= W1;
-        if (xr < 0) { if (!g.ghost_w) { zero |= mpos; xr = 0; } }
-        else if (xr >= g.nx) { if (!g.ghost_e) { zero |= !mpos; xr = g.nx - 1; } }
-        pz[j] = zero;
-        pxo[j] = (int64_t)(xr + a.psi_h) * pp + c;
-        axo[j] = (int64_t)(xr + a.avg_in_h) * ap + c;
-        own[j] = write_avg && xi < W1 && xg >= ox0 && xg < ox1;
-        oxo[j] = (int64_t)(xg + a.avg_out_h) * op + c;
+    for (int i = 0; i < NI; ++i) {
+        const int e = tid + i * NT;
+        const int xi = e / G4, q = e % G4;
+        const int xg = x0s - L + xi, cc = c0 + q * VEC;
+        own_ptr[i] = (write_avg && e < W1 * G4 && cc < g.C && xg >= ox0 && xg < ox1)
+                         ? a.avg_out + fidx(xg, 0, cc, g.ny, a.avg_out_h, g.C) : nullptr;
     }
-
-    auto issue_row = [&](int yy, int b) {     // pbar lead row y = yy into buffer b
-        Real* base = s1 + (size_t)b * 2 * FS;
-        bool yz = false;
-        int yr = yy;
-        if (yr < 0) { yz = npos; yr = 0; }
-        else if (yr >= g.ny) { yz = !npos; yr = g.ny - 1; }
-        const int64_t prow = (int64_t)(yr + a.psi_h) * g.C;
-        const int64_t arow = (int64_t)(yr + a.avg_in_h) * g.C;
-#pragma unroll
-        for (int j = 0; j < NX; ++j) {
-            const int xi = ty + j * KT;
-            if (xi < W1) {
-                const bool ok = !(pz[j] || yz);
-                cp_async<sizeof(Real)>(base + xi * PG_CC + tx, a.psi + (ok ? pxo[j] + prow : 0), ok);
-                if (ema)
-                    cp_async<sizeof(Real)>(base + FS + xi * PG_CC + tx,
-                                           a.avg_in + (ok ? axo[j] + arow : 0), ok);
-            }
-        }
-    };
 
     Real r1g[T], r1m[T];   // stage-1 x pass of pbar (by pbar row)
     Real c1x[T], c1y[T];   // psi_x, psi_y (by row)
@@ -364,7 +310,7 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
 
 #pragma unroll
     for (int k = 0; k < S - 1; ++k) {
-        if (k < nsteps) issue_row(vs + L + k, k);
+        if (k < nsteps) st.issue(vs + L + k, sbase + k * NF * FSB, FSB);
         cp_async_commit();
     }
     int step = 0;
@@ -374,16 +320,27 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
             const int v = v0 + s;
             const int yl = v + L;                  // pbar lead row (y coords)
             cp_async_wait<S - 2>();
-            Real* buf = s1 + (size_t)(step % S) * 2 * FS;
-            const bool own_row = yl >= oy0 && yl < oy1;
+            Real* buf = s1 + (size_t)(step % S) * NF * FS;
+            if (EMA || write_avg) {                // form pbar on own items; write back owned
+                const bool own_row = yl >= oy0 && yl < oy1;
 #pragma unroll
-            for (int j = 0; j < NX; ++j) {         // form pbar on own elements
-                const int xi = ty + j * KT;
-                if (xi < W1) {
-                    Real pv = buf[xi * PG_CC + tx];
-                    if (ema) pv = buf[FS + xi * PG_CC + tx] * a.omt + a.theta * pv;
-                    buf[xi * PG_CC + tx] = pv;
-                    if (own[j] && own_row) a.avg_out[oxo[j] + (int64_t)(yl + a.avg_out_h) * g.C] = pv;
+                for (int i = 0; i < NI; ++i) {
+                    const int e = tid + i * NT;
+                    if (e < W1 * G4) {
+                        Real* p = buf + (e / G4) * PG_CC + (e % G4) * VEC;
+                        Real pv[VEC];
+#pragma unroll
+                        for (int vv = 0; vv < VEC; ++vv) {
+                            pv[vv] = p[vv];
+                            if (EMA) pv[vv] = p[FS + vv] * omt + theta * pv[vv];
+                            p[vv] = pv[vv];
+                        }
+                        if (own_ptr[i] && own_row) {
+                            Real* o = own_ptr[i] + (int64_t)yl * g.C;
+#pragma unroll
+                            for (int vv = 0; vv < VEC; ++vv) o[vv] = pv[vv];
+                        }
+                    }
                 }
             }
             __syncthreads();
@@ -411,7 +368,8 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
                 s2b[ty * PG_CC + tx] = px;
                 s2b[(KT + ty) * PG_CC + tx] = py;
             }
-            if (step + S - 1 < nsteps) issue_row(vs + L + step + S - 1, (step + S - 1) % S);
+            if (step + S - 1 < nsteps)
+                st.issue(vs + L + step + S - 1, sbase + ((step + S - 1) % S) * NF * FSB, FSB);
             cp_async_commit();
             ++step;
             __syncthreads();
@@ -425,7 +383,7 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
                 }
                 r2x[(s + L) % T] = mx;
                 r2y[(s + L) % T] = my;
-                if (xout && cval && v >= ua && v < ub) {
+                if (xout && v >= ua && v < ub) {
                     Real mmx = 0, mmy = 0;
 #pragma unroll
                     for (int b = 0; b < T; ++b) {
@@ -435,14 +393,15 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
                     const Real px = c1x[s % T], py = c1y[s % T];
                     const Real rx = ar_mu * (mmx - px);
                     const Real ry = ar_nu * (mmy - py);
-                    Real kx = nanmin(kxmax,
-                                     nanmin(fast_div(a_abs * fabs(rx) * dx, eps + fabs(px)),
-                                            fast_div(a_sq * (rx * rx) * dx, eps + amu * (px * px))));
-                    Real ky = nanmin(kymax,
-                                     nanmin(fast_div(a_abs * fabs(ry) * dy, eps + fabs(py)),
-                                            fast_div(a_sq * (ry * ry) * dy, eps + anu * (py * py))));
-                    if (!isfinite(kx)) kx = Real(0);
-                    if (!isfinite(ky)) ky = Real(0);
+                    // min(dx|mu|, min(a_abs|R|dx/(eps+|p|), a_sq R^2 dx/(eps+|mu| p^2))), where a
+                    // NaN candidate makes the result NaN and then 0 (numpy minimum +
+                    // nan_to_num); dx|mu| is finite, so the min itself is never +-inf.
+                    const Real bx = fast_div(cabs_x * fabs(rx), eps + fabs(px));
+                    const Real sx = fast_div(csq_x * (rx * rx), eps + amu * (px * px));
+                    const Real by = fast_div(cabs_y * fabs(ry), eps + fabs(py));
+                    const Real sy = fast_div(csq_y * (ry * ry), eps + anu * (py * py));
+                    const Real kx = (bx != bx || sx != sx) ? Real(0) : fmin(kxmax, fmin(bx, sx));
+                    const Real ky = (by != by || sy != sy) ? Real(0) : fmin(kymax, fmin(by, sy));
                     const int64_t o = fidx(xs, v - L, c, g.ny, a.k_h, g.C);
                     a.kx[o] = kx;
                     a.ky[o] = ky;
