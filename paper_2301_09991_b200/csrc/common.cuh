@@ -76,40 +76,29 @@ __device__ __forceinline__ void cp_async_s(unsigned saddr, const void* gmem, boo
 // (cell, VEC-channel group) and stages that vector of every field, so the thread
 // that owns an item can post-process it (psi - delta, the EMA) right after its own
 // copies land.  Everything row independent — shared address, x resolution of the
-// vacuum rule, x part of the global offset — is computed once; per row only the y
-// rule and one multiply-add per field remain.
+// vacuum rule, the field pointer at (x, y = 0) — is computed once; per row only the
+// y rule, one multiply per field kind and an address add per field remain.
 //   kind 0 field (psi-like): vacuum rule (zero on incoming sides, else clamp);
-//   kind 1 field (k-like):   stored on the +-L band, zero outside it, never clamped.
+//   kind 1 field (k-like):   stored on the +-band, zero outside it, never clamped.
+// KMASK bit f = kind of field f.
 struct FieldDesc {
     const void* ptr;   // nullptr: field reads as 0
     int halo;
-    int kind;
 };
 
-template <class Real, int VEC, int NI, int NF>
+template <class Real, int VEC, int NI, int NF, int KMASK>
 struct Stager {
+    const Real* base[NI][NF];   // field pointer at (x storage, y = 0), nullptr = zero in x
     unsigned soff[NI];          // shared byte offset of the item (field 0, buffer 0)
-    int64_t xoff[NI][NF];       // element offset of (x storage, y storage 0, channel)
-    bool xz[NI][NF];            // zero because of x (or invalid channel / no item)
     bool npos[NI];
-    bool item[NI];              // this thread has an item in slot i
+    bool item[NI];
     int ny, C, band;
-    int halo[NF];
-    int kind[NF];
-    const Real* ptr[NF];
 
-    // x0: global x of staged cell 0; W cells; c0: first channel of the CTA
     __device__ __forceinline__ void init(const Geo& g, const FieldDesc* fd, int x0, int W,
                                          int c0, int band_, const Real* mu, const Real* nu,
                                          int tid, int nthreads) {
         constexpr int G4 = 32 / VEC;
         ny = g.ny; C = g.C; band = band_;
-#pragma unroll
-        for (int f = 0; f < NF; ++f) {
-            ptr[f] = (const Real*)fd[f].ptr;
-            halo[f] = fd[f].halo;
-            kind[f] = fd[f].kind;
-        }
 #pragma unroll
         for (int i = 0; i < NI; ++i) {
             const int e = tid + i * nthreads;
@@ -127,20 +116,25 @@ struct Stager {
             for (int f = 0; f < NF; ++f) {
                 bool z = !cval || fd[f].ptr == nullptr;
                 int xr = xg;
-                if (fd[f].kind == 0) {
+                if (!((KMASK >> f) & 1)) {
                     if (xr < 0) { if (!g.ghost_w) { z |= mp; xr = 0; } }
                     else if (xr >= g.nx) { if (!g.ghost_e) { z |= !mp; xr = g.nx - 1; } }
                 } else {
                     z |= xg < -band || xg >= g.nx + band;
                 }
-                xz[i][f] = z;
-                xoff[i][f] = (int64_t)(xr + fd[f].halo) * (int64_t)(g.ny + 2 * fd[f].halo) * g.C + c;
+                const int h = fd[f].halo;
+                base[i][f] = z ? nullptr
+                               : (const Real*)fd[f].ptr +
+                                     ((int64_t)(xr + h) * (g.ny + 2 * h) + h) * (int64_t)g.C + c;
             }
         }
     }
 
     // stage row yy into the buffer at shared address sbuf (field stride fstride bytes)
-    __device__ __forceinline__ void issue(int yy, unsigned sbuf, unsigned fstride) const {
+    __device__ __forceinline__ void issue(int yy, unsigned sbuf, unsigned fstride,
+                                          const Real* dummy) const {
+        const bool yz1 = yy < -band || yy >= ny + band;
+        const int off1 = yy * C;
 #pragma unroll
         for (int i = 0; i < NI; ++i) {
             if (!item[i]) continue;
@@ -148,12 +142,12 @@ struct Stager {
             int yr = yy;
             if (yr < 0) { yz0 = npos[i]; yr = 0; }
             else if (yr >= ny) { yz0 = !npos[i]; yr = ny - 1; }
-            const bool yz1 = yy < -band || yy >= ny + band;
+            const int off0 = yr * C;
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
-                const bool z = xz[i][f] || (kind[f] == 0 ? yz0 : yz1);
-                const int ys = (kind[f] == 0 ? yr : yy) + halo[f];
-                const Real* src = z ? ptr[0] : ptr[f] + xoff[i][f] + (int64_t)ys * C;
+                const bool k1 = (KMASK >> f) & 1;
+                const bool z = base[i][f] == nullptr || (k1 ? yz1 : yz0);
+                const Real* src = z ? dummy : base[i][f] + (k1 ? off1 : off0);
                 cp_async_s<VEC * (int)sizeof(Real)>(sbuf + f * fstride + soff[i], src, !z);
             }
         }

@@ -74,10 +74,15 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
     constexpr int T = 2 * L + 1;
     constexpr int W = PG_TX + 2 * L;
     constexpr int NT = PG_CC * PG_TX;
-    constexpr int NI = (W * (PG_CC / VEC) + NT - 1) / NT;   // staged items per thread
+    constexpr int G4 = PG_CC / VEC;
+    constexpr int NI = (W * G4 + NT - 1) / NT;     // staged items per thread
     constexpr int NF = SWEEP ? 4 : 3;              // psi, kx, ky (, delta)
     constexpr int S = PGStages<Real>::value;       // rows in flight
     constexpr int FS = W * PG_CC;                  // elements per field row
+    // centre values of the output row (staged L steps earlier) ride in register rings:
+    // the smem ring only holds the rows in flight
+    constexpr bool CSM = false;
+    constexpr int TC = T;
     extern __shared__ __align__(16) unsigned char smraw[];
     Real* sm = reinterpret_cast<Real*>(smraw);
     __shared__ double red[32];
@@ -90,25 +95,35 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
     const bool cval = c < g.C;
     const int cs = cval ? c : g.C - 1;
     const int n = cs / g.ng, gg = cs - n * g.ng;
-    const Real mu = a.mu[n], nu = a.nu[n];
-    const Real mu_dx = mu * a.inv_dx, nu_dy = nu * a.inv_dy;
+    const Real mu_dx = a.mu[n] * a.inv_dx, nu_dy = a.nu[n] * a.inv_dy;
+    const Real hx = a.hx, hy = a.hy;
     const int x0 = blockIdx.x * PG_TX;
     const int x = x0 + ty;
     const int ya = blockIdx.z * a.ly;
     const int yb = min(g.ny, ya + a.ly);
-    const bool xval = x < g.nx;
+    const bool act = x < g.nx && cval;
     const int nsteps = 2 * L + (int)(((yb - ya) + T - 1) / T) * T;   // lead rows ya-L ...
 
-    FieldDesc fd[4] = {{a.psi, a.psi_h, 0}, {a.kx, a.k_h, 1}, {a.ky, a.k_h, 1},
-                       {a.delta, a.delta_h, 0}};
-    Stager<Real, VEC, NI, NF> st;
+    FieldDesc fd[4] = {{a.psi, a.psi_h}, {a.kx, a.k_h}, {a.ky, a.k_h}, {a.delta, a.delta_h}};
+    Stager<Real, VEC, NI, NF, 0x6> st;
     st.init(g, fd, x0 - L, W, c0, L, a.mu, a.nu, tid, NT);
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(sm);
     constexpr unsigned FSB = FS * sizeof(Real);
 
-    // x-pass rings (by row mod T), unit taps
-    Real rgx[T], rmx[T], rsx[T], rsk[T], rkx[T], rmk[T], rky[T];
-    Real cp[T], ckx[T], cky[T];
+    // epilogue pointers at y = 0 (per output only y * stride is added)
+    const int xs = act ? x : 0;
+    const int64_t cell0 = (int64_t)xs * g.ny;
+    const Real* sig_p = a.sigma + cell0 * g.ng + gg;
+    const int qst = a.q_per_dof ? g.C : g.ng;
+    const Real* q_p = a.q + cell0 * qst + (a.q_per_dof ? c : gg);
+    Real* o_p = SWEEP ? a.out + fidx(xs, 0, cs, g.ny, a.out_h, g.C)
+                      : (a.r ? a.r + fidx(xs, 0, cs, g.ny, a.r_h, g.C) : nullptr);
+    const Real dscale = a.beta, strm = a.strm ? a.strm[n] : Real(0);
+
+    // x-pass rings (by row mod T): A = mu/dx G psi + hx S(kx psi) (M_y later),
+    // S psi, S kx (M_y), M psi (G_y and S_y), M(ky psi), M ky (S_y)
+    Real ra[T], rsx[T], rkx[T], rmx[T], rmk[T], rky[T];
+    Real cp[TC], ckx[TC], cky[TC];
 
 #define PG_STEP(K, SLOT)                                                             \
     {                                                                                \
@@ -118,8 +133,8 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
         if (SWEEP) {                                                                 \
             _Pragma("unroll") for (int i = 0; i < NI; ++i) {                         \
                 const int e = tid + i * NT;                                          \
-                if (e < W * (PG_CC / VEC)) {                                         \
-                    Real* p_ = buf_ + (e / (PG_CC / VEC)) * PG_CC + (e % (PG_CC / VEC)) * VEC; \
+                if (e < W * G4) {                                                    \
+                    Real* p_ = buf_ + (e / G4) * PG_CC + (e % G4) * VEC;             \
                     _Pragma("unroll") for (int v = 0; v < VEC; ++v) p_[v] -= p_[3 * FS + v]; \
                 }                                                                    \
             }                                                                        \
@@ -138,28 +153,28 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
             a_mk += Real(TP::m(t_)) * (p_ * k2_);                                    \
             a_ky += Real(TP::m(t_)) * k2_;                                           \
         }                                                                            \
-        rgx[SLOT] = a_g; rmx[SLOT] = a_m; rsx[SLOT] = a_s; rsk[SLOT] = a_sk;         \
-        rkx[SLOT] = a_k; rmk[SLOT] = a_mk; rky[SLOT] = a_ky;                         \
-        cp[SLOT] = buf_[(ty + L) * PG_CC + tx];                                      \
-        ckx[SLOT] = buf_[FS + (ty + L) * PG_CC + tx];                                \
-        cky[SLOT] = buf_[2 * FS + (ty + L) * PG_CC + tx];                            \
+        ra[SLOT] = mu_dx * a_g + hx * a_sk;                                          \
+        rsx[SLOT] = a_s; rkx[SLOT] = a_k; rmx[SLOT] = a_m;                           \
+        rmk[SLOT] = a_mk; rky[SLOT] = a_ky;                                          \
+        if (!CSM) {                                                                  \
+            cp[(SLOT) % TC] = buf_[(ty + L) * PG_CC + tx];                           \
+            ckx[(SLOT) % TC] = buf_[FS + (ty + L) * PG_CC + tx];                     \
+            cky[(SLOT) % TC] = buf_[2 * FS + (ty + L) * PG_CC + tx];                 \
+        }                                                                            \
         if (k_ + S - 1 < nsteps)                                                     \
-            st.issue(ya - L + k_ + S - 1, sbase + ((k_ + S - 1) % S) * NF * FSB, FSB); \
+            st.issue(ya - L + k_ + S - 1, sbase + ((k_ + S - 1) % S) * NF * FSB, FSB, a.psi); \
         cp_async_commit();                                                           \
     }
 
 #pragma unroll
     for (int k = 0; k < S - 1; ++k) {
-        if (k < nsteps) st.issue(ya - L + k, sbase + k * NF * FSB, FSB);
+        if (k < nsteps) st.issue(ya - L + k, sbase + k * NF * FSB, FSB, a.psi);
         cp_async_commit();
     }
     // prologue: lead rows ya-L .. ya+L-1 (ya is a multiple of T)
 #pragma unroll
     for (int k = 0; k < 2 * L; ++k) PG_STEP(k, (k - L + T) % T);
 
-    const Real beta = a.beta, hx = a.hx, hy = a.hy;
-    const Real strm = a.strm ? a.strm[n] : Real(0);
-    const int64_t cell0 = (int64_t)(xval ? x : 0) * g.ny;
     double l1 = 0.0;
     int kbase = 2 * L;
     for (int y0 = ya; y0 < yb; y0 += T, kbase += T) {
@@ -167,32 +182,35 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
         for (int s = 0; s < T; ++s) {
             const int y = y0 + s;
             PG_STEP(kbase + s, (s + L) % T);
-            if (y < yb && xval && cval) {
-                Real px = 0, py = 0, kxp = 0, kxkp = 0, kxk = 0, kykp = 0, kyp = 0, kyk = 0;
+            if (act && y < yb) {
+                Real pa = 0, kxp = 0, kxk = 0, py = 0, kyp = 0, kykp = 0, kyk = 0;
 #pragma unroll
                 for (int b = 0; b < T; ++b) {
                     const int sl = (s - L + b + T) % T;
-                    px += Real(TP::m(b)) * rgx[sl];
-                    py += Real(TP::g(b)) * rmx[sl];
+                    pa += Real(TP::m(b)) * ra[sl];
                     kxp += Real(TP::m(b)) * rsx[sl];
-                    kxkp += Real(TP::m(b)) * rsk[sl];
                     kxk += Real(TP::m(b)) * rkx[sl];
-                    kykp += Real(TP::s(b)) * rmk[sl];
+                    py += Real(TP::g(b)) * rmx[sl];
                     kyp += Real(TP::s(b)) * rmx[sl];
+                    kykp += Real(TP::s(b)) * rmk[sl];
                     kyk += Real(TP::s(b)) * rky[sl];
                 }
-                const Real pc = cp[s], kxc = ckx[s], kyc = cky[s];
-                const Real diffx = hx * ((kxkp + kxc * kxp) - pc * kxk);
-                const Real diffy = hy * ((kykp + kyc * kyp) - pc * kyk);
-                const int64_t cell = cell0 + y;
-                const Real sig = a.sigma[cell * g.ng + gg];
-                const Real qq = a.q_per_dof ? a.q[cell * g.C + c] : a.q[cell * g.ng + gg];
-                const Real r = (((mu_dx * px + nu_dy * py) + diffx) + diffy) + sig * pc - qq;
-                if (SWEEP) {
-                    const Real d = beta * (strm + sig);
-                    a.out[fidx(x, y, c, g.ny, a.out_h, g.C)] = pc - fast_div(r, d);
+                Real pc, kxc, kyc;
+                if (CSM) {   // staged buffer of this output row (lead row L steps ago)
+                    const Real* cb = sm + (size_t)((kbase + s - L) % S) * NF * FS + (ty + L) * PG_CC + tx;
+                    pc = cb[0]; kxc = cb[FS]; kyc = cb[2 * FS];
                 } else {
-                    if (a.r) a.r[fidx(x, y, c, g.ny, a.r_h, g.C)] = r;
+                    pc = cp[s % TC]; kxc = ckx[s % TC]; kyc = cky[s % TC];
+                }
+                // r = mu psi_x + nu psi_y + hx[K(kx psi) + kx K psi - psi K kx] + hy[...] + sig psi - q
+                const Real sig = sig_p[y * g.ng];
+                const Real r = (((pa + hx * (kxc * kxp - pc * kxk)) + nu_dy * py) +
+                                hy * ((kykp + kyc * kyp) - pc * kyk)) +
+                               sig * pc - q_p[y * qst];
+                if (SWEEP) {
+                    o_p[(int64_t)y * g.C] = pc - fast_div(r, dscale * (strm + sig));
+                } else {
+                    if (o_p) o_p[(int64_t)y * g.C] = r;
                     l1 += fabs((double)r);
                 }
             }
@@ -288,8 +306,8 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
     const int vs = ua - PRE;
     const int nsteps = PRE + (int)(((ub - ua) + T - 1) / T) * T;
 
-    FieldDesc fd[2] = {{a.psi, a.psi_h, 0}, {a.avg_in, a.avg_in_h, 0}};
-    Stager<Real, VEC, NI, NF> st;
+    FieldDesc fd[2] = {{a.psi, a.psi_h}, {a.avg_in, a.avg_in_h}};
+    Stager<Real, VEC, NI, NF, 0> st;
     st.init(g, fd, x0s - L, W1, c0, 0, a.mu, a.nu, tid, NT);
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(s1);
     constexpr unsigned FSB = FS * sizeof(Real);
@@ -310,7 +328,7 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
 
 #pragma unroll
     for (int k = 0; k < S - 1; ++k) {
-        if (k < nsteps) st.issue(vs + L + k, sbase + k * NF * FSB, FSB);
+        if (k < nsteps) st.issue(vs + L + k, sbase + k * NF * FSB, FSB, a.psi);
         cp_async_commit();
     }
     int step = 0;
@@ -369,7 +387,7 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
                 s2b[(KT + ty) * PG_CC + tx] = py;
             }
             if (step + S - 1 < nsteps)
-                st.issue(vs + L + step + S - 1, sbase + ((step + S - 1) % S) * NF * FSB, FSB);
+                st.issue(vs + L + step + S - 1, sbase + ((step + S - 1) % S) * NF * FSB, FSB, a.psi);
             cp_async_commit();
             ++step;
             __syncthreads();
