@@ -34,10 +34,16 @@ struct PGStages { static constexpr int value = sizeof(Real) == 4 ? 4 : 3; };
 
 template <class Real>
 __device__ __forceinline__ Real fast_div(Real a, Real b) { return a / b; }
-template <>
-__device__ __forceinline__ float fast_div<float>(float a, float b) {
-    return a * __frcp_rn(b);      // correctly rounded reciprocal, then one rounding more
+// fp32: MUFU reciprocal + one Newton step (<= 1 ulp, no slow-path call); the divisors
+// here are positive and finite except in diverging iterates, where NaN -> 0 downstream
+// matches the reference's inf/inf -> NaN -> 0.
+__device__ __forceinline__ float rcp_nr(float b) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b));
+    return fmaf(fmaf(-b, r, 1.0f), r, r);
 }
+template <>
+__device__ __forceinline__ float fast_div<float>(float a, float b) { return a * rcp_nr(b); }
 
 // ---------------------------------------------------------------------------------
 // K3 / K5: PG residual  r = mu psi_x + nu psi_y + diff_x + diff_y + sigma psi - q
@@ -304,7 +310,8 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
 
     constexpr int PRE = ((4 * L + T - 1) / T) * T;
     const int vs = ua - PRE;
-    const int nsteps = PRE + (int)(((ub - ua) + T - 1) / T) * T;
+    const int nsteps = PRE + (int)(((ub + 1 - ua) + T - 1) / T) * T;   // +1: stage-2 lag
+    const int64_t kbase_o = fidx(xout ? xs : 0, 0, cs, g.ny, a.k_h, g.C);
 
     FieldDesc fd[2] = {{a.psi, a.psi_h}, {a.avg_in, a.avg_in_h}};
     Stager<Real, VEC, NI, NF, 0> st;
@@ -326,13 +333,16 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
     Real c1x[T], c1y[T];   // psi_x, psi_y (by row)
     Real r2x[T], r2y[T];   // M_x psi_x, M_x psi_y (by row)
 
+    // Step v stages pbar row y = v + L, runs stage 1 at band row v + L and stage 2 on
+    // the stage-1 row of step v - 1 (band row v - 1 + L), emitting k at band row v - 1.
+    // The barrier of step v publishes both the staged row and step v-1's stage-1 row.
 #pragma unroll
     for (int k = 0; k < S - 1; ++k) {
         if (k < nsteps) st.issue(vs + L + k, sbase + k * NF * FSB, FSB, a.psi);
         cp_async_commit();
     }
     int step = 0;
-    for (int v0 = vs; v0 < ub; v0 += T) {
+    for (int v0 = vs; v0 <= ub; v0 += T) {
 #pragma unroll
         for (int s = 0; s < T; ++s) {
             const int v = v0 + s;
@@ -362,7 +372,8 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
                 }
             }
             __syncthreads();
-            Real* s2b = s2 + (size_t)(step & 1) * 2 * KT * PG_CC;
+            Real* s2w = s2 + (size_t)(step & 1) * 2 * KT * PG_CC;         // this step's row
+            const Real* s2r = s2 + (size_t)((step + 1) & 1) * 2 * KT * PG_CC;  // previous
             {   // stage 1 at band row v + L (y = v)
                 Real ag = 0, am = 0;
 #pragma unroll
@@ -383,32 +394,28 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
                 py *= inv_dy;
                 c1x[(s + L) % T] = px;
                 c1y[(s + L) % T] = py;
-                s2b[ty * PG_CC + tx] = px;
-                s2b[(KT + ty) * PG_CC + tx] = py;
+                s2w[ty * PG_CC + tx] = px;
+                s2w[(KT + ty) * PG_CC + tx] = py;
             }
-            if (step + S - 1 < nsteps)
-                st.issue(vs + L + step + S - 1, sbase + ((step + S - 1) % S) * NF * FSB, FSB, a.psi);
-            cp_async_commit();
-            ++step;
-            __syncthreads();
-            // stage 2: x pass (mass) at band row v + L, y pass (mass) -> row v
+            // stage 2: x pass (mass) at band row v - 1 + L, y pass (mass) -> row v - 1
             if (s2thr) {
                 Real mx = 0, my = 0;
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
-                    mx += Real(TP::m(t)) * s2b[(ty - L + t) * PG_CC + tx];
-                    my += Real(TP::m(t)) * s2b[(KT + ty - L + t) * PG_CC + tx];
+                    mx += Real(TP::m(t)) * s2r[(ty - L + t) * PG_CC + tx];
+                    my += Real(TP::m(t)) * s2r[(KT + ty - L + t) * PG_CC + tx];
                 }
-                r2x[(s + L) % T] = mx;
-                r2y[(s + L) % T] = my;
-                if (xout && v >= ua && v < ub) {
+                r2x[(s - 1 + L + T) % T] = mx;
+                r2y[(s - 1 + L + T) % T] = my;
+                const int vo = v - 1;
+                if (xout && vo >= ua && vo < ub) {
                     Real mmx = 0, mmy = 0;
 #pragma unroll
                     for (int b = 0; b < T; ++b) {
-                        mmx += Real(TP::m(b)) * r2x[(s - L + b + T) % T];
-                        mmy += Real(TP::m(b)) * r2y[(s - L + b + T) % T];
+                        mmx += Real(TP::m(b)) * r2x[(s - 1 - L + b + 2 * T) % T];
+                        mmy += Real(TP::m(b)) * r2y[(s - 1 - L + b + 2 * T) % T];
                     }
-                    const Real px = c1x[s % T], py = c1y[s % T];
+                    const Real px = c1x[(s - 1 + T) % T], py = c1y[(s - 1 + T) % T];
                     const Real rx = ar_mu * (mmx - px);
                     const Real ry = ar_nu * (mmy - py);
                     // min(dx|mu|, min(a_abs|R|dx/(eps+|p|), a_sq R^2 dx/(eps+|mu| p^2))), where a
@@ -420,11 +427,15 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
                     const Real sy = fast_div(csq_y * (ry * ry), eps + anu * (py * py));
                     const Real kx = (bx != bx || sx != sx) ? Real(0) : fmin(kxmax, fmin(bx, sx));
                     const Real ky = (by != by || sy != sy) ? Real(0) : fmin(kymax, fmin(by, sy));
-                    const int64_t o = fidx(xs, v - L, c, g.ny, a.k_h, g.C);
+                    const int64_t o = kbase_o + (int64_t)(vo - L) * g.C;
                     a.kx[o] = kx;
                     a.ky[o] = ky;
                 }
             }
+            if (step + S - 1 < nsteps)
+                st.issue(vs + L + step + S - 1, sbase + ((step + S - 1) % S) * NF * FSB, FSB, a.psi);
+            cp_async_commit();
+            ++step;
         }
     }
     cp_async_wait<0>();
