@@ -127,13 +127,20 @@ def options_for(P, pd, dtype, cycles=None):
     return P.SolverOptions(**o, pg=P.PGConfig(**(pg or {})), dtype=dtype)
 
 
+def per_dof_bytes(kernel, esz):
+    return {"pg_sweep": 5, "pg_residual": 4, "pg_residual+ema": 6, "pg_diffusivity": 5,
+            "ema": 3, "upwind_residual": 2}.get(kernel, 0) * esz
+
+
 def bytes_model(pd, hier, live):
     """Algorithmic fp32 bytes per cycle."""
     n0 = pd.dof()
     coarse = sum(l.grid.nx * l.grid.ny * l.quad.n_dir * pd.n_groups for l in hier.levels[1:])
     if pd.options["scheme"] == "upwind" or pd.options.get("pg", {}).get("alpha_r", 3.0) == 0.0:
         return 28 * n0 + 16 * coarse
-    return (64 if live else 56) * n0 + 16 * coarse
+    # live: K2 20 + K3 16 + finest correction 8 + K5 20; frozen: the EMA (12 B standalone)
+    # shares the residual's psi read (R/multigrid.py:282 then :287), 8 B -> 52
+    return (64 if live else 52) * n0 + 16 * coarse
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -277,9 +284,11 @@ def run_b200(args, rank, world, local_rank):
     kernel_stats = {}
     for k, ts in probe.items():
         kernel_stats[k] = {"ms_avg": float(np.mean(ts)), "launches": len(ts)}
+        if per_dof_bytes(k, esz):
+            kernel_stats[k]["GBps"] = per_dof_bytes(k, esz) * dof / (np.mean(ts) * 1e-3) / 1e9
     dominant = "pg_sweep" if "pg_sweep" in probe else "correction"
-    per_dof = {"pg_sweep": 5 * esz, "pg_residual": 4 * esz, "pg_diffusivity": 5 * esz,
-               "ema": 3 * esz, "correction": None}
+    per_dof = {"pg_sweep": 5 * esz, "pg_residual": 4 * esz, "pg_residual+ema": 6 * esz,
+               "pg_diffusivity": 5 * esz, "ema": 3 * esz, "correction": None}
     roof = None
     if dominant in probe and per_dof.get(dominant):
         ms_k = float(np.mean(probe[dominant]))

@@ -119,6 +119,8 @@ int csn_pg_diffusivities(int dtype, int order, const csn_geom* g, const double* 
 /* R/discretisation.py:227-276 pg_residual (anisotropy "xy", given diffusivities),
  * two modes:
  *   residual (psi_out == NULL): r = pg_residual(psi) -> r (interior), l1 (device, nullable);
+ *            optionally fused with the iterate average of frozen-diffusivity cycles
+ *            (R/multigrid.py:217-225, in place on avg: avg_mode 1 copy, 2 EMA, 0 off);
  *   sweep    (psi_out != NULL): R/multigrid.py:301-304 fused — psi' = psi - delta
  *            (delta nullable), psi_out = psi' - pg_residual(psi') / (beta (|mu|/dx + |nu|/dy
  *            + sigma)) (R/multigrid.py:159-172).  psi_out must not alias psi.
@@ -129,7 +131,8 @@ int csn_pg_residual(int dtype, int order, const csn_geom* g, const double* taps,
                     const void* sigma, const void* q, int q_per_dof,
                     const void* mu, const void* nu, const void* strm,
                     void* r, int r_halo, void* psi_out, int psi_out_halo, double beta,
-                    double* partials, double* l1, void* stream);
+                    double* partials, double* l1, void* avg, int avg_halo, int avg_mode,
+                    double theta, void* stream);
 
 /* R/grid.py:193-198 scalar_flux: phi (device fp64 [nx][ny][ng]) = sum_n w_n psi. */
 int csn_scalar_flux(int dtype, const csn_geom* g, const void* psi, int halo,

@@ -45,7 +45,7 @@ _SIGNATURES = {
                               _c_int, _c_dbl, _vp, _vp, _vp, _vp, _c_int, _vp], _c_int),
     "csn_pg_residual": ([_c_int, _c_int, _GP, _DP, _vp, _c_int, _vp, _c_int, _vp, _vp, _c_int,
                          _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _c_int, _vp, _c_int, _c_dbl,
-                         _vp, _vp, _vp], _c_int),
+                         _vp, _vp, _vp, _c_int, _c_int, _c_dbl, _vp], _c_int),
     "csn_scalar_flux": ([_c_int, _GP, _vp, _c_int, _vp, _vp, _vp], _c_int),
     "csn_group_source": ([_c_int, _GP, _vp, _vp, _vp, _vp, _c_dbl, _vp, _vp, _vp, _vp], _c_int),
     "csn_fission_source": ([_GP, _vp, _vp, _vp, _c_dbl, _vp, _vp], _c_int),

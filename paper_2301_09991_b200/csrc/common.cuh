@@ -84,6 +84,7 @@ __device__ __forceinline__ void cp_async_s(unsigned saddr, const void* gmem, boo
 struct FieldDesc {
     const void* ptr;   // nullptr: field reads as 0
     int halo;
+    int xlo = -(1 << 30), xhi = 1 << 30;   // stage only cells with xlo <= x < xhi
 };
 
 template <class Real, int VEC, int NI, int NF, int KMASK>
@@ -114,7 +115,7 @@ struct Stager {
             const int xg = x0 + xi;
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
-                bool z = !cval || fd[f].ptr == nullptr;
+                bool z = !cval || fd[f].ptr == nullptr || xg < fd[f].xlo || xg >= fd[f].xhi;
                 int xr = xg;
                 if (!((KMASK >> f) & 1)) {
                     if (xr < 0) { if (!g.ghost_w) { z |= mp; xr = 0; } }

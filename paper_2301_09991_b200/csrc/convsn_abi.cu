@@ -66,12 +66,12 @@ inline bool vec_ok(const csn_geom* g, int vec) {
     return C % vec == 0 && face % vec == 0 && 8 * face == C;
 }
 
-template <class Real, int L, bool SWEEP, int VEC>
+template <class Real, int L, int MODE, int VEC>
 void launch_pg_resid(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<Real>& a) {
-    constexpr size_t sm = pg_residual_smem<Real, L, SWEEP>();
+    constexpr size_t sm = pg_residual_smem<Real, L, MODE>();
     static bool attr = false;
-    if (!attr) { set_smem(pg_residual_kernel<Real, L, SWEEP, VEC>, sm); attr = true; }
-    pg_residual_kernel<Real, L, SWEEP, VEC><<<grid, block, sm, st>>>(a);
+    if (!attr) { set_smem(pg_residual_kernel<Real, L, MODE, VEC>, sm); attr = true; }
+    pg_residual_kernel<Real, L, MODE, VEC><<<grid, block, sm, st>>>(a);
 }
 
 template <class Real, int L, bool EMA, int VEC>
@@ -88,11 +88,15 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
                      const void* delta, int delta_h, const void* kx, const void* ky, int k_h,
                      const void* sigma, const void* q, int q_per_dof, const void* mu,
                      const void* nu, const void* strm, void* r, int r_h, void* out, int out_h,
-                     double beta, double* partials, double* l1, cudaStream_t st) {
+                     double beta, double* partials, double* l1, void* avg, int avg_h, int avg_mode,
+                     double theta, cudaStream_t st) {
     constexpr int T = 2 * L + 1;
     if (k_h < L) return CSN_E_ARG;
     if (!taps_match<L>(taps)) return CSN_E_ARG;
+    if (avg_mode < 0 || avg_mode > 2 || (avg_mode && (!avg || out))) return CSN_E_ARG;
     PGResidArgs<Real> a;
+    a.avg = (Real*)avg; a.avg_h = avg_h; a.avg_mode = avg ? avg_mode : 0;
+    a.theta = (Real)theta; a.omt = (Real)(1.0 - theta);
     a.g = make_geo(*g);
     a.psi = (const Real*)psi; a.psi_h = psi_h;
     a.delta = (const Real*)delta; a.delta_h = delta_h;
@@ -110,14 +114,20 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
     a.partials = (l1 || partials) ? partials : nullptr;
     dim3 grid(gx, gy, gz), block(PG_CC, PG_TX);
     const bool vec = vec_ok(g, 16 / (int)sizeof(Real));
+    constexpr int V = 16 / sizeof(Real);
     if (out) {
-        if (vec) launch_pg_resid<Real, L, true, 16 / sizeof(Real)>(grid, block, st, a);
-        else launch_pg_resid<Real, L, true, 1>(grid, block, st, a);
+        if (vec) launch_pg_resid<Real, L, PG_SWEEP, V>(grid, block, st, a);
+        else launch_pg_resid<Real, L, PG_SWEEP, 1>(grid, block, st, a);
         CSN_CHECK_LAUNCH();
     } else {
         if (l1 && !partials) return CSN_E_ARG;
-        if (vec) launch_pg_resid<Real, L, false, 16 / sizeof(Real)>(grid, block, st, a);
-        else launch_pg_resid<Real, L, false, 1>(grid, block, st, a);
+        if (a.avg_mode) {
+            if (vec) launch_pg_resid<Real, L, PG_RESID_EMA, V>(grid, block, st, a);
+            else launch_pg_resid<Real, L, PG_RESID_EMA, 1>(grid, block, st, a);
+        } else {
+            if (vec) launch_pg_resid<Real, L, PG_RESID, V>(grid, block, st, a);
+            else launch_pg_resid<Real, L, PG_RESID, 1>(grid, block, st, a);
+        }
         CSN_CHECK_LAUNCH();
         if (l1) {
             sum_f64_kernel<<<1, 1024, 0, st>>>(partials, (int64_t)gx * gy * gz, 1.0, l1);
@@ -390,14 +400,15 @@ int csn_pg_residual(int dtype, int order, const csn_geom* g, const double* taps,
                     const void* kx, const void* ky, int k_halo, const void* sigma, const void* q,
                     int q_per_dof, const void* mu, const void* nu, const void* strm, void* r,
                     int r_halo, void* psi_out, int psi_out_halo, double beta, double* partials,
-                    double* l1, void* stream) {
+                    double* l1, void* avg, int avg_halo, int avg_mode, double theta,
+                    void* stream) {
     if (!geom_ok(g) || !taps || !psi || !kx || !ky || !sigma || !q || !mu || !nu)
         return CSN_E_ARG;
     if (psi_out && (!strm || psi_out == psi)) return CSN_E_ARG;
     if (dtype != CSN_F32 && dtype != CSN_F64) return CSN_E_DTYPE;
     ORDER_DISPATCH(pg_residual_impl, g, taps, psi, psi_halo, delta, delta_halo, kx, ky, k_halo,
                    sigma, q, q_per_dof, mu, nu, strm, r, r_halo, psi_out, psi_out_halo, beta,
-                   partials, l1, S(stream));
+                   partials, l1, avg, avg_halo, avg_mode, theta, S(stream));
 }
 
 int csn_scalar_flux(int dtype, const csn_geom* g, const void* psi, int halo, const void* w,

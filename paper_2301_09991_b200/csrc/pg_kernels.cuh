@@ -65,24 +65,31 @@ struct PGResidArgs {
     Real* r; int r_h;
     Real* out; int out_h; Real beta;
     double* partials;
+    Real* avg; int avg_h; int avg_mode; Real theta, omt;   // fused EMA (frozen cycles)
     int ly;             // y rows per CTA chunk, multiple of T
 };
 
-template <class Real, int L, bool SWEEP>
+// residual kernel modes: plain residual, residual + fused iterate EMA, fused sweep
+constexpr int PG_RESID = 0, PG_RESID_EMA = 1, PG_SWEEP = 2;
+
+template <class Real, int L, int MODE>
 constexpr size_t pg_residual_smem() {
-    return (size_t)PGStages<Real>::value * (SWEEP ? 4 : 3) * (PG_TX + 2 * L) * PG_CC * sizeof(Real);
+    return (size_t)PGStages<Real>::value * (MODE == PG_RESID ? 3 : 4) * (PG_TX + 2 * L) * PG_CC *
+           sizeof(Real);
 }
 
-template <class Real, int L, bool SWEEP, int VEC>
+template <class Real, int L, int MODE, int VEC>
 __global__ void __launch_bounds__(PG_CC * PG_TX, (sizeof(Real) == 4 && L <= 3) ? 2 : 1)
 pg_residual_kernel(const PGResidArgs<Real> a) {
+    constexpr bool SWEEP = MODE == PG_SWEEP;
+    constexpr bool EMA = MODE == PG_RESID_EMA;
     using TP = UnitTaps<L>;
     constexpr int T = 2 * L + 1;
     constexpr int W = PG_TX + 2 * L;
     constexpr int NT = PG_CC * PG_TX;
     constexpr int G4 = PG_CC / VEC;
     constexpr int NI = (W * G4 + NT - 1) / NT;     // staged items per thread
-    constexpr int NF = SWEEP ? 4 : 3;              // psi, kx, ky (, delta)
+    constexpr int NF = MODE == PG_RESID ? 3 : 4;   // psi, kx, ky (, delta | pbar)
     constexpr int S = PGStages<Real>::value;       // rows in flight
     constexpr int FS = W * PG_CC;                  // elements per field row
     // centre values of the output row (staged L steps earlier) ride in register rings:
@@ -110,7 +117,9 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
     const bool act = x < g.nx && cval;
     const int nsteps = 2 * L + (int)(((yb - ya) + T - 1) / T) * T;   // lead rows ya-L ...
 
-    FieldDesc fd[4] = {{a.psi, a.psi_h}, {a.kx, a.k_h}, {a.ky, a.k_h}, {a.delta, a.delta_h}};
+    FieldDesc fd[4] = {{a.psi, a.psi_h}, {a.kx, a.k_h}, {a.ky, a.k_h},
+                       {SWEEP ? a.delta : a.avg, SWEEP ? a.delta_h : a.avg_h}};
+    if (EMA) { fd[3].xlo = x0; fd[3].xhi = min(x0 + PG_TX, g.nx); }   // owned columns only
     Stager<Real, VEC, NI, NF, 0x6> st;
     st.init(g, fd, x0 - L, W, c0, L, a.mu, a.nu, tid, NT);
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(sm);
@@ -125,6 +134,18 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
     Real* o_p = SWEEP ? a.out + fidx(xs, 0, cs, g.ny, a.out_h, g.C)
                       : (a.r ? a.r + fidx(xs, 0, cs, g.ny, a.r_h, g.C) : nullptr);
     const Real dscale = a.beta, strm = a.strm ? a.strm[n] : Real(0);
+    // fused iterate averaging (R/multigrid.py:217-225) on the interior cells this CTA
+    // owns: elementwise, so in place; psi and pbar_old arrive through the staging ring
+    Real* avg_p[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+        const int e = tid + i * NT;
+        const int xi = e / G4, cc = c0 + (e % G4) * VEC;
+        const int xg = x0 - L + xi;
+        avg_p[i] = (EMA && e < W * G4 && cc < g.C && xi >= L && xi < L + PG_TX && xg < g.nx)
+                       ? a.avg + fidx(xg, 0, cc, g.ny, a.avg_h, g.C) : nullptr;
+    }
+    const int oy0 = max(ya, 0), oy1 = yb;
 
     // x-pass rings (by row mod T): A = mu/dx G psi + hx S(kx psi) (M_y later),
     // S psi, S kx (M_y), M psi (G_y and S_y), M(ky psi), M ky (S_y)
@@ -142,6 +163,20 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
                 if (e < W * G4) {                                                    \
                     Real* p_ = buf_ + (e / G4) * PG_CC + (e % G4) * VEC;             \
                     _Pragma("unroll") for (int v = 0; v < VEC; ++v) p_[v] -= p_[3 * FS + v]; \
+                }                                                                    \
+            }                                                                        \
+        } else if (EMA) {                                                            \
+            const int yl_ = ya - L + k_;                                             \
+            if (yl_ >= oy0 && yl_ < oy1) {                                           \
+                _Pragma("unroll") for (int i = 0; i < NI; ++i) {                     \
+                    if (avg_p[i]) {                                                  \
+                        const int e = tid + i * NT;                                  \
+                        const Real* p_ = buf_ + (e / G4) * PG_CC + (e % G4) * VEC;   \
+                        Real* o_ = avg_p[i] + (int64_t)yl_ * g.C;                    \
+                        _Pragma("unroll") for (int v = 0; v < VEC; ++v)              \
+                            o_[v] = a.avg_mode == 2 ? p_[3 * FS + v] * a.omt + a.theta * p_[v] \
+                                                    : p_[v];                         \
+                    }                                                                \
                 }                                                                    \
             }                                                                        \
         }                                                                            \

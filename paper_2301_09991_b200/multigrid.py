@@ -432,12 +432,13 @@ class CycleEngine:
         if scheme == "pg":
             if fs is None:
                 raise ValueError("the pg scheme needs the filter set fs")
-            kx, ky = self._diffusivities(psi, fs, cfg, pg_state)
+            kx, ky, ema = self._diffusivities(psi, fs, cfg, pg_state)
             t = self._t0()
             pg_residual_launch(psi, None, None, f.quad, fs, kx, ky, g.halo, r=self.r0, r_halo=0,
                                partials=self.partials, l1=self.l1, sigma=self.sigma[0], qt=qt,
-                               per_dof=per_dof, consts=c0)
-            self._t1("pg_residual", t)
+                               per_dof=per_dof, consts=c0, avg=ema[0], avg_mode=ema[1],
+                               theta=ema[2])
+            self._t1("pg_residual" if ema[1] == 0 else "pg_residual+ema", t)
         elif scheme == "upwind":
             t = self._t0()
             _lib.call("csn_upwind_residual", dt, self.geoms[0], _lib.ptr(d), g.halo,
@@ -491,7 +492,7 @@ class CycleEngine:
                 self.k_scratch = (torch.zeros_like(d), torch.zeros_like(d))
             kx, ky = self.k_scratch
             diffusivities_into(d, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky, g.halo)
-            return kx, ky
+            return kx, ky, (None, 0, 1.0)
         need_k = pg_state.diffusivities is None or not pg_state.frozen
         if need_k and pg_state.diffusivities is None:
             pg_state.diffusivities = (torch.zeros_like(d), torch.zeros_like(d))
@@ -499,32 +500,30 @@ class CycleEngine:
         if pg_state.avg_theta >= 1.0:
             if need_k:
                 diffusivities_into(d, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky, g.halo)
-            return kx, ky
+            return kx, ky, (None, 0, 1.0)
         pg_state._avg_quad = self.h.levels[0].quad
         first = pg_state._avg is None
         if first:
             pg_state._avg = torch.empty_like(d)
             pg_state._avg_grid = g
+        if not need_k:
+            # frozen diffusivities: the EMA rides in the residual kernel (elementwise, in place)
+            return kx, ky, (pg_state._avg, 1 if first else 2, float(pg_state.avg_theta))
         t = self._t0()
-        if need_k:
-            if first:
-                diffusivities_into(d, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky, g.halo,
-                                   avg_out=pg_state._avg, avg_mode=1)
-            else:
-                if pg_state._avg_spare is None or pg_state._avg_spare.shape != d.shape:
-                    pg_state._avg_spare = torch.empty_like(d)
-                out = pg_state._avg_spare
-                diffusivities_into(d, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky, g.halo,
-                                   avg_in=pg_state._avg, avg_out=out, avg_mode=2,
-                                   theta=pg_state.avg_theta)
-                pg_state._avg_spare = pg_state._avg
-                pg_state._avg = out
+        if first:
+            diffusivities_into(d, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky, g.halo,
+                               avg_out=pg_state._avg, avg_mode=1)
         else:
-            _lib.call("csn_ema", _lib.dtype_code(d), self.geoms[0], _lib.ptr(pg_state._avg),
-                      g.halo, _lib.ptr(d), g.halo, float(pg_state.avg_theta), 1 if first else 2,
-                      _lib.stream())
-        self._t1("pg_diffusivity" if need_k else "ema", t)
-        return kx, ky
+            if pg_state._avg_spare is None or pg_state._avg_spare.shape != d.shape:
+                pg_state._avg_spare = torch.empty_like(d)
+            out = pg_state._avg_spare
+            diffusivities_into(d, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky, g.halo,
+                               avg_in=pg_state._avg, avg_out=out, avg_mode=2,
+                               theta=pg_state.avg_theta)
+            pg_state._avg_spare = pg_state._avg
+            pg_state._avg = out
+        self._t1("pg_diffusivity", t)
+        return kx, ky, (None, 0, 1.0)
 
 
 def sawtooth_cycle(psi, q, hierarchy, fs=None, cfg=None, scheme="pg", n_sweeps=3, pg_sweeps=1,
