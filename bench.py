@@ -69,7 +69,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -209,8 +209,8 @@ def run_b200(args, rank, world, local_rank):
     import torch
     import paper_2301_09991_b200 as P
     from paper_2301_09991_b200 import _lib
+    from paper_2301_09991_b200.eigen import Solver
     from paper_2301_09991_b200.problems import problem_from_data
-    from paper_2301_09991_b200.eigen import _buffers
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -219,39 +219,25 @@ def run_b200(args, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
     pd = workload(args.config, args.nx)
-    cycles_total = args.warmup + args.steps
-    opts = options_for(P, pd, args.dtype, cycles_total)
+    total = args.warmup + args.steps
+    eigen = pd.driver == "power_iteration"
+    inner = pd.inner_iters or 1
+    opts = options_for(P, pd, args.dtype, None if eigen else total)
+    if eigen:
+        opts.outer_iters = -(-total // inner)
     prob = problem_from_data(pd)
-    setup = P.setup_transport(prob, opts)
-    g = setup.grid
-    ng = pd.n_groups
+    solver = Solver(prob, opts, inner if eigen else None)
+    eng = solver.eng
+    graphs = args.graphs == "on" or (args.graphs == "auto" and args.config not in ("c4", "c5w"))
+    eng.use_graphs = graphs
     dtype = opts.torch_dtype()
-    psi = P.Field(g, setup.quad.n_dir, ng, dtype=dtype, device=dev)
-    eng = setup.hierarchy.engine(ng, dtype, dev)
-    bufs = _buffers(setup, dtype, dev)
-    pgs = P.PGState(opts.k_avg_theta) if opts.scheme == "pg" else None
-    fission = None
-    # per-cycle source assembly exactly as _run_cycles does it
-    from paper_2301_09991_b200.eigen import assemble_group_source
-    from paper_2301_09991_b200.grid import scalar_flux_into
-    one_group = ng == 1
-
-    def one_cycle():
-        if not one_group:
-            scalar_flux_into(psi, setup.quad, bufs.phi)
-            assemble_group_source(bufs.phi, setup.mat, 0.0, dtype, bufs.q, fission)
-        return eng.cycle(psi, bufs.q, setup.filters, opts.pg, opts.scheme, opts.jacobi_sweeps,
-                         opts.pg_sweeps, pgs)
-
-    if one_group:
-        bufs.phi.zero_()
-        assemble_group_source(bufs.phi, setup.mat, 0.0, dtype, bufs.q, fission)
     hist = []
-    frozen_before = []
     for _ in range(args.warmup):
-        hist.append(one_cycle())
-    # ---- timed region: K cycles, device-timed with events, clocks sampled
-    eng.probe = {}
+        hist.append(solver.step())
+    # ---- timed region: K cycles, device-timed with CUDA events, clocks sampled
+    probe_live = not graphs          # per-kernel events inside the timed region (eager path)
+    eng.probe = {} if probe_live else None
+    frozen_before = []
     sampler = ClockSampler(local_rank)
     torch.cuda.synchronize()
     if dist is not None:
@@ -261,8 +247,8 @@ def run_b200(args, rank, world, local_rank):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     for _ in range(args.steps):
-        frozen_before.append(bool(pgs.frozen) if pgs is not None else False)
-        hist.append(one_cycle())
+        frozen_before.append(bool(solver.pgs.frozen))
+        hist.append(solver.step())
     ev1.record()
     torch.cuda.synchronize()
     n_launch = lib.csn_launch_count() - n_launch0
@@ -273,7 +259,18 @@ def run_b200(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
-    probe = {k: [a.elapsed_time(b) for a, b in v] for k, v in eng.probe.items()}
+    kernel_timing = "CUDA events around each launch inside the timed region (eager launches)"
+    if not probe_live:               # graphs in the timed region: break down in an eager pass
+        eng.use_graphs = False
+        eng.probe = {}
+        extra = Solver(prob, opts, inner if eigen else None)
+        extra.eng.use_graphs = False
+        extra.eng.probe = eng.probe
+        for _ in range(min(total, args.warmup + 3)):
+            extra.step()
+        kernel_timing = ("CUDA events, eager pass of the first W+3 cycles after the timed "
+                         "region (the timed region replays CUDA graphs)")
+    probe = {k: [a.elapsed_time(b) for a, b in v] for k, v in (eng.probe or {}).items()}
     eng.probe = None
     dof = pd.dof()
     value = dof * args.steps * world / (ms * 1e-3)
@@ -286,22 +283,29 @@ def run_b200(args, rank, world, local_rank):
         kernel_stats[k] = {"ms_avg": float(np.mean(ts)), "launches": len(ts)}
         if per_dof_bytes(k, esz):
             kernel_stats[k]["GBps"] = per_dof_bytes(k, esz) * dof / (np.mean(ts) * 1e-3) / 1e9
-    dominant = "pg_sweep" if "pg_sweep" in probe else "correction"
-    per_dof = {"pg_sweep": 5 * esz, "pg_residual": 4 * esz, "pg_residual+ema": 6 * esz,
-               "pg_diffusivity": 5 * esz, "ema": 3 * esz, "correction": None}
+    dominant = "pg_sweep" if "pg_sweep" in probe else "upwind_residual"
     roof = None
-    if dominant in probe and per_dof.get(dominant):
+    if dominant in probe:
         ms_k = float(np.mean(probe[dominant]))
-        achieved = per_dof[dominant] * dof / (ms_k * 1e-3) / 1e9
+        bpl = per_dof_bytes(dominant, esz) * dof
+        achieved = bpl / (ms_k * 1e-3) / 1e9
+        traffic = committed_traffic(args.config, dominant, args.dtype)
         roof = {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak,
-                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback 6.65 TB/s",
-                "traffic": None,
-                "bytes_per_launch": per_dof[dominant] * dof, "ms_per_launch": ms_k,
-                "share_of_step": ms_k * len(probe[dominant]) / ms}
+                "peak_source": ("measured (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
+                                else "fallback 6.65 TB/s"),
+                "traffic": traffic, "bytes_per_launch": bpl, "ms_per_launch": ms_k,
+                "share_of_step": ms_k * len(probe[dominant]) / (sum(sum(v) for v in probe.values()) or 1),
+                "timing": kernel_timing}
+        if pd.options.get("order", 1) >= 3:
+            flops = (32 * (2 * pd.options["order"] + 1) + 22) * dof
+            fp32_peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+            roof["fp32"] = {"tflops": flops / (ms_k * 1e-3) / 1e12, "peak_tflops": fp32_peak,
+                            "frac": flops / (ms_k * 1e-3) / 1e12 / fp32_peak,
+                            "note": "p=3 sits past the FP32 ridge (~9 F/B): 32T+22 flops/DOF vs 20 B/DOF"}
     live = sum(1 for f in frozen_before if not f)
-    b_cycle = (bytes_model(pd, setup.hierarchy, True) * live
-               + bytes_model(pd, setup.hierarchy, False) * (args.steps - live)) / args.steps
+    b_cycle = (bytes_model(pd, solver.setup.hierarchy, True) * live
+               + bytes_model(pd, solver.setup.hierarchy, False) * (args.steps - live)) / args.steps
     cycle_roof = b_cycle / (ms / args.steps * 1e-3) / 1e9
 
     # ---- end to end through the public API with host buffers (rank-local)
@@ -309,14 +313,14 @@ def run_b200(args, rank, world, local_rank):
     if not args.no_e2e:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = P.solve_fixed_source(prob, opts) if pd.driver == "fixed_source" else \
-            P.power_iteration(prob, opts, inner_iters=pd.inner_iters)
+        res = P.solve_fixed_source(prob, opts) if not eigen else \
+            P.power_iteration(prob, opts, inner_iters=inner)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         ncyc = len(res.residual_history)
-        mf = setup.mat
+        mf = solver.setup.mat
         h2d = sum(a.nbytes for a in (mf.sigma_s, mf.source, mf.nu_sigma_f, mf.chi))
-        h2d += sum(l.sigma_t.size * esz for l in setup.hierarchy.levels)
+        h2d += sum(l.sigma_t.size * esz for l in solver.setup.hierarchy.levels)
         d2h = res.phi.nbytes + 8 * ncyc
         e2e = {"value": dof * ncyc * world / wall, "unit": "DOF-updates/s",
                "h2d_bytes_per_step": h2d / ncyc, "d2h_bytes_per_step": d2h / ncyc,
@@ -339,17 +343,15 @@ def run_b200(args, rank, world, local_rank):
             "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if dtype == torch.float32 else "f64",
             "data": "synthetic (seeded BASELINE generators, paper_2301_09991_b200/benchmarks.py)",
-            "config": {"workload": f"{args.config}: " + {
-                "c4": "1 group, cubic PG, 512x512 cells, 2048 ordinates (n_a=16), 32x32 seeded blocks",
-                "c2": "1 group, quadratic PG, 128x128 cells, 512 ordinates, 8x8 seeded blocks",
-                "c1": "1 group, linear, PG off (alpha_r=0), 64x64, 128 ordinates",
-                "c3": "2-group eigen, linear PG, 256x256, 512 ordinates",
-                "c5w": "7-group eigen, linear PG, 512x512 per GPU, 2048 ordinates"}.get(args.config, ""),
-                "dof_per_cycle": dof, "nx": pd.nx, "ny": pd.ny, "ordinates": 8 * pd.n_a ** 2,
-                "groups": ng, "order": pd.options["order"], "levels": setup.hierarchy.n_levels,
-                "live_cycles": live, "frozen_cycles": args.steps - live,
-                "l2": "fields 2.3 GB >> 126 MB L2 (no flush needed)" if args.config == "c4" else "see DESIGN.md",
-                "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+            "config": {"workload": f"{args.config}: " + WORKLOADS.get(args.config, ""),
+                       "dof_per_cycle": dof, "nx": pd.nx, "ny": pd.ny,
+                       "ordinates": 8 * pd.n_a ** 2, "groups": pd.n_groups,
+                       "order": pd.options["order"], "scheme": pd.options["scheme"],
+                       "levels": solver.setup.hierarchy.n_levels, "live_cycles": live,
+                       "frozen_cycles": args.steps - live, "cuda_graphs": graphs,
+                       "l2": "per-cycle fields >> 126 MB L2 (no flush needed)"
+                       if dof * esz > 4 * 126e6 else "fields partly L2-resident; see DESIGN.md",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
             "roofline": roof,
             "cycle_roofline": {"bytes_per_cycle": b_cycle, "achieved": cycle_roof, "peak": peak,
                                "unit": "GB/s", "frac": cycle_roof / peak},
@@ -360,7 +362,28 @@ def run_b200(args, rank, world, local_rank):
             "clocks": clocks,
             "residual_history": hist,
         }
+        if eigen:
+            line["k_history"] = solver.k_history
         print(json.dumps(line), flush=True)
+
+
+WORKLOADS = {
+    "c4": "1 group, cubic PG, 512x512 cells, 2048 ordinates (n_a=16), 32x32 seeded blocks",
+    "c2": "1 group, quadratic PG, 128x128 cells, 512 ordinates, 8x8 seeded blocks",
+    "c1": "1 group, linear, PG off (alpha_r=0), 64x64, 128 ordinates",
+    "c3": "2-group k-eigenvalue, linear PG, 256x256, 512 ordinates, 5 cycles per outer",
+    "c5w": "7-group k-eigenvalue, linear PG, 512x512 per GPU, 2048 ordinates, 3 cycles per outer",
+}
+
+
+def committed_traffic(config, kernel, dtype):
+    """dram read+write bytes per launch of `kernel` from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(f"{config}:{kernel}:{dtype}")
+    except (OSError, ValueError):
+        return None
 
 
 def main():
@@ -374,6 +397,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--graphs", default="auto", choices=["auto", "on", "off"])
     args = ap.parse_args()
     if args.warmup < 0 or args.steps < 1:
         raise SystemExit("need --steps >= 1")

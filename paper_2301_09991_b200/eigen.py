@@ -190,8 +190,8 @@ def _run_cycles(psi, setup, n_iters, fission_frozen=None, pg_state=None, scheme=
     eng = setup.hierarchy.engine(psi.n_group, d.dtype, d.device)
     one_group = setup.mat.n_groups == 1
     if one_group:
-        bufs.phi.zero_()
-        assemble_group_source(bufs.phi, setup.mat, 0.0, d.dtype, bufs.q, fission_frozen)
+        assemble_group_source(torch.zeros_like(bufs.phi), setup.mat, 0.0, d.dtype, bufs.q,
+                              fission_frozen)
     history = []
     for _ in range(n_iters):
         if not one_group:
@@ -212,92 +212,176 @@ def _phi_host(psi, quad):
     return bufs_phi
 
 
+def _scale(t, s):
+    _lib.call("csn_scale", _lib.dtype_code(t), _lib.ptr(t), t.numel(), float(s), 1, _lib.stream())
+
+
+class Solver:
+    """Step-wise driver: one ``step()`` = one sawtooth cycle of the reference's solve.
+
+    Mirrors R/eigen.py:159-251: fixed-source problems run the bootstrap (upwind) cycles
+    then ``mg_iters`` cycles with a ``PGState``; fissile problems run power iteration,
+    freezing the fission source per outer (``inner_iters`` cycles) and applying the
+    production-ratio k update + rescale after each outer.  ``solve_fixed_source`` and
+    ``power_iteration`` are ``Solver(...).run()``; the benchmark times ``step()``.
+    """
+
+    def __init__(self, problem, options=None, inner_iters=None, setup=None):
+        self.options = options = options or SolverOptions()
+        self.setup = setup = setup or setup_transport(problem, options)
+        self.dtype = options.torch_dtype()
+        self.dev = default_device()
+        mat = setup.mat
+        self.eigen = bool(mat.fissile)
+        g = setup.grid
+        ng = mat.n_groups
+        self.psi = Field(g, setup.quad.n_dir, ng, dtype=self.dtype, device=self.dev)
+        self.bufs = _buffers(setup, self.dtype, self.dev)
+        self.eng = setup.hierarchy.engine(ng, self.dtype, self.dev)
+        self.pgs = PGState(options.k_avg_theta)
+        self.history = []            # residual history of the main (PG-state) cycles
+        self.boot_history = []
+        self.k = 1.0
+        self.k_history = [1.0]
+        self.empty = False
+        n_boot = options.bootstrap() if options.scheme == "pg" else 0
+        if self.eigen:
+            self.inner = options.mg_iters if inner_iters is None else inner_iters
+            self.md = mat.device(self.dev)
+            self.gm = _lib.geom(g.nx, g.ny, 1, ng, 1, g.dx, g.dy)
+            self.psi.fill(1.0)
+            apply_boundary(self.psi, setup.quad)
+            scalar_flux_into(self.psi, setup.quad, self.bufs.phi)
+            prod = self._production()
+            if prod <= 0.0:
+                raise ValueError("initial fission production is zero")
+            _scale(self.psi.data, prod)
+            _scale(self.bufs.phi, prod)
+            self.phases = [("boot", n_boot)] + [("outer", self.inner)] * options.outer_iters
+        else:
+            self.empty = not mat.source.any()
+            self.phases = [] if self.empty else [("boot", n_boot), ("main", options.mg_iters)]
+        self.phases = [ph for ph in self.phases if ph[1] > 0]
+        self.phase = 0
+        self.in_phase = 0
+        self.stopped = False
+        self.outer_done = 0
+
+    # ------------------------------------------------------------------ pieces
+    def _production(self):
+        _production_dev(self.bufs.phi, self.setup.mat, self.setup.grid.dx, self.setup.grid.dy,
+                        self.bufs.prod, self.bufs.partials)
+        return float(self.bufs.prod.item())
+
+    def _frozen_fission(self, inv_k):
+        _lib.call("csn_fission_source", self.gm, _lib.ptr(self.bufs.phi), _lib.ptr(self.md["chi"]),
+                  _lib.ptr(self.md["nu_sigma_f"]), float(inv_k), _lib.ptr(self.bufs.fission),
+                  _lib.stream())
+        return self.bufs.fission
+
+    def _source(self, fission, new_block):
+        """q for this cycle (R/eigen.py:145-148).
+
+        One group: the in-scatter term sum_a s[a->g] phi_a - s[g->g] phi_g is
+        identically 0, so q = s (+ frozen fission) is assembled once per block.
+        """
+        setup, b = self.setup, self.bufs
+        if setup.mat.n_groups == 1:
+            if new_block or not getattr(self, "_q_ready", False):
+                if not hasattr(self, "_zphi"):
+                    self._zphi = torch.zeros_like(b.phi)
+                assemble_group_source(self._zphi, setup.mat, 0.0, self.dtype, b.q, fission)
+                self._q_ready = True
+            return b.q
+        scalar_flux_into(self.psi, setup.quad, b.phi)
+        assemble_group_source(b.phi, setup.mat, 0.0, self.dtype, b.q, fission)
+        return b.q
+
+    @property
+    def done(self):
+        return self.stopped or self.phase >= len(self.phases)
+
+    def step(self):
+        """Run one cycle (plus the outer update when an outer completes); returns res."""
+        if self.done:
+            raise RuntimeError("solve already finished")
+        kind, n = self.phases[self.phase]
+        opts = self.options
+        boot = kind == "boot"
+        fission = None
+        if self.eigen:
+            if self.in_phase == 0:       # freeze the fission source of this block
+                self._fis = self._frozen_fission(1.0 if boot else 1.0 / self.k)
+            fission = self._fis
+        q = self._source(fission, self.in_phase == 0)
+        res = self.eng.cycle(self.psi, q, self.setup.filters, opts.pg,
+                             "upwind" if boot else opts.scheme, opts.jacobi_sweeps,
+                             opts.pg_sweeps, None if boot else self.pgs)
+        (self.boot_history if boot else self.history).append(res)
+        self.in_phase += 1
+        finite = math.isfinite(res)
+        if self.in_phase >= n or not finite:
+            if self.eigen and kind == "outer":
+                self._outer_update()
+            self.phase += 1
+            self.in_phase = 0
+            if not finite and not self.eigen:
+                # R/eigen.py:154-155 stops the block; fixed source then ends
+                self.stopped = kind == "main"
+        return res
+
+    def _outer_update(self):
+        """k <- k P; psi, phi, psi_avg /= P (R/eigen.py:238-248)."""
+        scalar_flux_into(self.psi, self.setup.quad, self.bufs.phi)
+        prod = self._production()
+        self.outer_done += 1
+        if not math.isfinite(prod) or prod <= 0.0:
+            raise ValueError(f"fission production became {prod} at outer iteration "
+                             f"{self.outer_done}")
+        self.k = self.k * prod
+        _scale(self.psi.data, prod)
+        _scale(self.bufs.phi, prod)
+        self.pgs.scale_average(prod)
+        self.k_history.append(self.k)
+
+    def run(self):
+        while not self.done:
+            self.step()
+        return self.result()
+
+    def result(self):
+        setup, ng = self.setup, self.setup.mat.n_groups
+        if self.eigen:
+            return EigenState(psi=self.psi, phi=self.bufs.phi.cpu().numpy(), k_eff=self.k,
+                              iteration=self.options.outer_iters, history=self.k_history,
+                              residual_history=self.history, pg_log=list(self.pgs.log))
+        if self.empty:
+            return FixedSourceResult(psi=self.psi, phi=np.zeros((setup.grid.nx, setup.grid.ny, ng)),
+                                     residual_history=[0.0], converged=True)
+        phi = _phi_host(self.psi, setup.quad).cpu().numpy()
+        hist = self.history
+        converged = True
+        if self.options.tol_rel > 0.0 and hist and hist[0] > 0.0:
+            converged = hist[-1] <= self.options.tol_rel * hist[0]
+        if hist and not np.isfinite(hist[-1]):
+            converged = False
+        return FixedSourceResult(psi=self.psi, phi=phi, residual_history=hist, converged=converged,
+                                 bootstrap_history=self.boot_history, pg_log=list(self.pgs.log))
+
+
 def solve_fixed_source(problem, options=None):
     """Source-driven multigrid solve (R/eigen.py:159-191)."""
     options = options or SolverOptions()
     setup = setup_transport(problem, options)
-    dtype = options.torch_dtype()
     if setup.mat.fissile:
         raise ValueError("problem has fission; use power_iteration")
-    dev = default_device()
-    ng = setup.mat.n_groups
-    if not setup.mat.source.any():
-        return FixedSourceResult(psi=Field(setup.grid, setup.quad.n_dir, ng, dtype=dtype, device=dev),
-                                 phi=np.zeros((setup.grid.nx, setup.grid.ny, ng)),
-                                 residual_history=[0.0], converged=True)
-    psi = Field(setup.grid, setup.quad.n_dir, ng, dtype=dtype, device=dev)
-    boot = []
-    if options.scheme == "pg" and options.bootstrap() > 0:
-        psi, boot = _run_cycles(psi, setup, options.bootstrap(), scheme="upwind")
-    pgs = PGState(options.k_avg_theta)
-    psi, history = _run_cycles(psi, setup, options.mg_iters, pg_state=pgs)
-    phi = _phi_host(psi, setup.quad).cpu().numpy()
-    converged = True
-    if options.tol_rel > 0.0 and history[0] > 0.0:
-        converged = history[-1] <= options.tol_rel * history[0]
-    if not np.isfinite(history[-1]):
-        converged = False
-    return FixedSourceResult(psi=psi, phi=phi, residual_history=history, converged=converged,
-                             bootstrap_history=boot, pg_log=list(pgs.log))
-
-
-def _scale(t, s):
-    _lib.call("csn_scale", _lib.dtype_code(t), _lib.ptr(t), t.numel(), float(s), 1, _lib.stream())
+    return Solver(problem, options, setup=setup).run()
 
 
 def power_iteration(problem, options=None, inner_iters=None):
     """Power method for k-effective (R/eigen.py:194-251)."""
     options = options or SolverOptions()
     setup = setup_transport(problem, options)
-    mat = setup.mat
-    dtype = options.torch_dtype()
-    if not mat.fissile:
+    if not setup.mat.fissile:
         raise ValueError("problem has no fission source; power iteration is undefined")
-    if inner_iters is None:
-        inner_iters = options.mg_iters
-    dev = default_device()
-    g = setup.grid
-    psi = Field(g, setup.quad.n_dir, mat.n_groups, dtype=dtype, device=dev).fill(1.0)
-    apply_boundary(psi, setup.quad)
-    bufs = _buffers(setup, dtype, dev)
-    phi = _phi_host(psi, setup.quad)
-    md = mat.device(dev)
-    gm = _lib.geom(g.nx, g.ny, 1, mat.n_groups, 1, g.dx, g.dy)
-
-    def production():
-        _production_dev(phi, mat, g.dx, g.dy, bufs.prod, bufs.partials)
-        return float(bufs.prod.item())
-
-    prod = production()
-    if prod <= 0.0:
-        raise ValueError("initial fission production is zero")
-    _scale(psi.data, prod)
-    _scale(phi, prod)
-    k = 1.0
-    history = [k]
-    residual_history = []
-    pgs = PGState(options.k_avg_theta)
-
-    def frozen(inv_k):
-        _lib.call("csn_fission_source", gm, _lib.ptr(phi), _lib.ptr(md["chi"]),
-                  _lib.ptr(md["nu_sigma_f"]), float(inv_k), _lib.ptr(bufs.fission), _lib.stream())
-        return bufs.fission
-
-    if options.scheme == "pg" and options.bootstrap() > 0:
-        psi, _ = _run_cycles(psi, setup, options.bootstrap(), fission_frozen=frozen(1.0),
-                             scheme="upwind")
-    for it in range(options.outer_iters):
-        psi, res = _run_cycles(psi, setup, inner_iters, fission_frozen=frozen(1.0 / k),
-                               pg_state=pgs)
-        residual_history.extend(res)
-        scalar_flux_into(psi, setup.quad, phi)
-        prod = production()
-        if not math.isfinite(prod) or prod <= 0.0:
-            raise ValueError(f"fission production became {prod} at outer iteration {it + 1}")
-        k = k * prod
-        _scale(psi.data, prod)
-        _scale(phi, prod)
-        pgs.scale_average(prod)
-        history.append(k)
-    return EigenState(psi=psi, phi=phi.cpu().numpy(), k_eff=k, iteration=options.outer_iters,
-                      history=history, residual_history=residual_history, pg_log=list(pgs.log))
+    return Solver(problem, options, inner_iters, setup=setup).run()

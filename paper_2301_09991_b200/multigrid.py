@@ -379,6 +379,11 @@ class CycleEngine:
         self.psi_alt = None
         self.k_scratch = None
         self.probe = None          # {kernel name: [(start event, end event)]} when timing
+        self.use_graphs = True     # replay recurring cycle plans from captured CUDA graphs
+        self._graphs = {}
+        self._seen = set()
+        self._cap_stream = None
+        self._graph_warm = False
 
     def _t0(self):
         if self.probe is None:
@@ -420,57 +425,43 @@ class CycleEngine:
     # ---------------------------------------------------------------- cycle
     def cycle(self, psi, q, fs=None, cfg=None, scheme="pg", n_sweeps=3, pg_sweeps=1,
               pg_state=None, sync=True):
-        """One sawtooth cycle in place; returns the fp64 L1 of the pre-update residual."""
+        """One sawtooth cycle in place; returns the fp64 L1 of the pre-update residual.
+
+        Host decisions (diffusivity refresh or frozen + fused EMA, buffer ping-pong) are
+        planned first; the kernel sequence is then issued eagerly, or — from the second
+        time the same plan and buffers recur — replayed from a captured CUDA graph.
+        """
         cfg = cfg or PGConfig()
-        L = self.h.levels
-        f = L[0]
+        if scheme not in ("pg", "upwind"):
+            raise ValueError(f"unknown scheme {scheme!r}")
+        if scheme == "pg" and fs is None:
+            raise ValueError("the pg scheme needs the filter set fs")
         d = psi.data
         g = psi.grid
-        dt = _lib.dtype_code(d)
-        c0 = self.consts[0]
         qt, per_dof = source_tensor(q, g.nx, g.ny, psi.n_dir, psi.n_group, d)
-        if scheme == "pg":
-            if fs is None:
-                raise ValueError("the pg scheme needs the filter set fs")
-            kx, ky, ema = self._diffusivities(psi, fs, cfg, pg_state)
-            t = self._t0()
-            pg_residual_launch(psi, None, None, f.quad, fs, kx, ky, g.halo, r=self.r0, r_halo=0,
-                               partials=self.partials, l1=self.l1, sigma=self.sigma[0], qt=qt,
-                               per_dof=per_dof, consts=c0, avg=ema[0], avg_mode=ema[1],
-                               theta=ema[2])
-            self._t1("pg_residual" if ema[1] == 0 else "pg_residual+ema", t)
-        elif scheme == "upwind":
-            t = self._t0()
-            _lib.call("csn_upwind_residual", dt, self.geoms[0], _lib.ptr(d), g.halo,
-                      _lib.ptr(self.sigma[0]), _lib.ptr(qt), per_dof, _lib.ptr(c0["mu"]),
-                      _lib.ptr(c0["nu"]), _lib.ptr(self.r0), 0, _lib.ptr(self.partials),
-                      _lib.ptr(self.l1), _lib.stream())
-            self._t1("upwind_residual", t)
+        plan = self._plan(psi, fs, cfg, scheme, pg_sweeps, pg_state)
+        key = plan["key"] + (qt.data_ptr(), per_dof, n_sweeps, scheme, id(fs), cfg)
+
+        def run():
+            self._launch(plan, g, qt, per_dof, fs, cfg, scheme, n_sweeps)
+
+        if self.use_graphs and self.probe is None:
+            if not self._graph_warm:      # one-time CUDA-graph machinery cost, off the cycle
+                self._graph_warm = True
+                self._capture(lambda: _lib.call("csn_scale", _lib.F64, _lib.ptr(self.l1), 1, 1.0,
+                                                0, _lib.stream())).replay()
+            graph = self._graphs.get(key)
+            if graph is None and key in self._seen:
+                graph = self._capture(run)
+                self._graphs[key] = graph
+            if graph is not None:
+                graph.replay()
+            else:
+                run()
+                self._seen.add(key)
         else:
-            raise ValueError(f"unknown scheme {scheme!r}")
-        self.res_host.copy_(self.l1, non_blocking=True)
-        t = self._t0()
-        delta = self.correction(self.r0, n_sweeps, cfg.beta_diag if scheme == "pg" else 1.0)
-        self._t1("correction", t)
-        if scheme == "pg" and pg_sweeps > 0:
-            for k in range(pg_sweeps):
-                if self.psi_alt is None or self.psi_alt.shape != d.shape:
-                    self.psi_alt = torch.empty_like(d)
-                out = self.psi_alt
-                t = self._t0()
-                pg_residual_launch(psi, None, None, f.quad, fs, kx, ky, g.halo, psi_out=out,
-                                   out_halo=g.halo, delta=delta if k == 0 else None,
-                                   delta_halo=0, beta=cfg.beta_diag, sigma=self.sigma[0], qt=qt,
-                                   per_dof=per_dof, consts=c0)
-                self._t1("pg_sweep", t)
-                self.psi_alt = psi.data
-                psi.data = out
-        else:
-            _lib.call("csn_sub_interior", dt, self.geoms[0], _lib.ptr(psi.data), g.halo,
-                      _lib.ptr(delta), 0, _lib.stream())
-        t = self._t0()
-        apply_boundary(psi, f.quad)
-        self._t1("boundary", t)
+            run()
+        self._commit(plan, psi, pg_state)
         if not sync:
             return None
         torch.cuda.current_stream().synchronize()
@@ -479,51 +470,134 @@ class CycleEngine:
             pg_state.observe(res, cfg.k_freeze_rel)
         return res
 
-    def _diffusivities(self, psi, fs, cfg, pg_state):
+    def _capture(self, run):
+        """Capture `run` into a CUDA graph on a side stream (no GC / cache flush, unlike
+        torch.cuda.graph); all buffers are preallocated, nothing allocates inside."""
+        graph = torch.cuda.CUDAGraph()
+        if self._cap_stream is None:
+            self._cap_stream = torch.cuda.Stream(device=self.device)
+        cur = torch.cuda.current_stream()
+        self._cap_stream.wait_stream(cur)
+        with torch.cuda.stream(self._cap_stream):
+            graph.capture_begin()
+            try:
+                run()
+            finally:
+                graph.capture_end()
+        cur.wait_stream(self._cap_stream)
+        return graph
+
+    def _plan(self, psi, fs, cfg, scheme, pg_sweeps, pg_state):
+        """Host-side decisions and buffer assignment of one cycle (no launches)."""
         d = psi.data
-        g = psi.grid
+        if self.psi_alt is None or self.psi_alt.shape != d.shape or self.psi_alt.dtype != d.dtype:
+            self.psi_alt = torch.empty_like(d)
+        plan = {"psi": d, "alt": self.psi_alt, "k2": None, "ema": (None, 0, 1.0),
+                "kx": None, "ky": None, "pg_sweeps": pg_sweeps if scheme == "pg" else 0}
+        if scheme == "pg":
+            l = fs.half_width
+            if psi.grid.halo < 3 * l:
+                raise ValueError(f"PG diffusivities need halo >= {3 * l}, field has {psi.grid.halo}")
+            if pg_state is None:
+                if self.k_scratch is None or self.k_scratch[0].shape != d.shape:
+                    self.k_scratch = (torch.zeros_like(d), torch.zeros_like(d))
+                plan["kx"], plan["ky"] = self.k_scratch
+                plan["k2"] = (None, None, 0, 1.0)
+            else:
+                need_k = pg_state.diffusivities is None or not pg_state.frozen
+                if pg_state.diffusivities is None:
+                    pg_state.diffusivities = (torch.zeros_like(d), torch.zeros_like(d))
+                plan["kx"], plan["ky"] = pg_state.diffusivities
+                if pg_state.avg_theta >= 1.0:
+                    if need_k:
+                        plan["k2"] = (None, None, 0, 1.0)
+                else:
+                    pg_state._avg_quad = self.h.levels[0].quad
+                    first = pg_state._avg is None
+                    if first:
+                        pg_state._avg = torch.empty_like(d)
+                        pg_state._avg_grid = psi.grid
+                    theta = float(pg_state.avg_theta)
+                    if not need_k:      # frozen: the EMA rides in the residual kernel
+                        plan["ema"] = (pg_state._avg, 1 if first else 2, theta)
+                    elif first:
+                        plan["k2"] = (None, pg_state._avg, 1, theta)
+                    else:
+                        if pg_state._avg_spare is None or pg_state._avg_spare.shape != d.shape:
+                            pg_state._avg_spare = torch.empty_like(d)
+                        plan["k2"] = (pg_state._avg, pg_state._avg_spare, 2, theta)
+                        plan["swap_avg"] = True
+        ema, k2 = plan["ema"], plan["k2"]
+        plan["key"] = (d.data_ptr(), self.psi_alt.data_ptr(),
+                       None if plan["kx"] is None else plan["kx"].data_ptr(),
+                       None if k2 is None else tuple(None if t is None or isinstance(t, (int, float))
+                                                     else t.data_ptr() for t in k2[:2]) + k2[2:],
+                       (None if ema[0] is None else ema[0].data_ptr(),) + ema[1:], plan["pg_sweeps"])
+        return plan
+
+    def _launch(self, plan, g, qt, per_dof, fs, cfg, scheme, n_sweeps):
+        """Issue the kernel sequence of a planned cycle on the current stream."""
+        L = self.h.levels
+        f = L[0]
         c0 = self.consts[0]
-        l = fs.half_width
-        if g.halo < 3 * l:
-            raise ValueError(f"PG diffusivities need halo >= {3 * l}, field has {g.halo}")
-        nd, ng, na = psi.n_dir, psi.n_group, self.h.levels[0].quad.n_a
-        if pg_state is None:
-            if self.k_scratch is None or self.k_scratch[0].shape != d.shape:
-                self.k_scratch = (torch.zeros_like(d), torch.zeros_like(d))
-            kx, ky = self.k_scratch
-            diffusivities_into(d, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky, g.halo)
-            return kx, ky, (None, 0, 1.0)
-        need_k = pg_state.diffusivities is None or not pg_state.frozen
-        if need_k and pg_state.diffusivities is None:
-            pg_state.diffusivities = (torch.zeros_like(d), torch.zeros_like(d))
-        kx, ky = pg_state.diffusivities
-        if pg_state.avg_theta >= 1.0:
-            if need_k:
-                diffusivities_into(d, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky, g.halo)
-            return kx, ky, (None, 0, 1.0)
-        pg_state._avg_quad = self.h.levels[0].quad
-        first = pg_state._avg is None
-        if first:
-            pg_state._avg = torch.empty_like(d)
-            pg_state._avg_grid = g
-        if not need_k:
-            # frozen diffusivities: the EMA rides in the residual kernel (elementwise, in place)
-            return kx, ky, (pg_state._avg, 1 if first else 2, float(pg_state.avg_theta))
-        t = self._t0()
-        if first:
-            diffusivities_into(d, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky, g.halo,
-                               avg_out=pg_state._avg, avg_mode=1)
+        psi_in = plan["psi"]
+        dt = _lib.dtype_code(psi_in)
+        view = Field.__new__(Field)
+        view.grid = g
+        view.data = psi_in
+        nd, ng, na = psi_in.shape[2], psi_in.shape[3], f.quad.n_a
+        if scheme == "pg":
+            kx, ky = plan["kx"], plan["ky"]
+            if plan["k2"] is not None:
+                avg_in, avg_out, mode, theta = plan["k2"]
+                t = self._t0()
+                diffusivities_into(psi_in, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky,
+                                   g.halo, avg_in=avg_in, avg_out=avg_out, avg_mode=mode,
+                                   theta=theta)
+                self._t1("pg_diffusivity", t)
+            ema = plan["ema"]
+            t = self._t0()
+            pg_residual_launch(view, None, None, f.quad, fs, kx, ky, g.halo, r=self.r0, r_halo=0,
+                               partials=self.partials, l1=self.l1, sigma=self.sigma[0], qt=qt,
+                               per_dof=per_dof, consts=c0, avg=ema[0], avg_mode=ema[1],
+                               theta=ema[2])
+            self._t1("pg_residual" if ema[1] == 0 else "pg_residual+ema", t)
         else:
-            if pg_state._avg_spare is None or pg_state._avg_spare.shape != d.shape:
-                pg_state._avg_spare = torch.empty_like(d)
-            out = pg_state._avg_spare
-            diffusivities_into(d, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky, g.halo,
-                               avg_in=pg_state._avg, avg_out=out, avg_mode=2,
-                               theta=pg_state.avg_theta)
-            pg_state._avg_spare = pg_state._avg
-            pg_state._avg = out
-        self._t1("pg_diffusivity", t)
-        return kx, ky, (None, 0, 1.0)
+            t = self._t0()
+            _lib.call("csn_upwind_residual", dt, self.geoms[0], _lib.ptr(psi_in), g.halo,
+                      _lib.ptr(self.sigma[0]), _lib.ptr(qt), per_dof, _lib.ptr(c0["mu"]),
+                      _lib.ptr(c0["nu"]), _lib.ptr(self.r0), 0, _lib.ptr(self.partials),
+                      _lib.ptr(self.l1), _lib.stream())
+            self._t1("upwind_residual", t)
+        self.res_host.copy_(self.l1, non_blocking=True)
+        t = self._t0()
+        delta = self.correction(self.r0, n_sweeps, cfg.beta_diag if scheme == "pg" else 1.0)
+        self._t1("correction", t)
+        bufs = (plan["psi"], plan["alt"])
+        if plan["pg_sweeps"] > 0:
+            for k in range(plan["pg_sweeps"]):
+                view.data = bufs[k % 2]
+                t = self._t0()
+                pg_residual_launch(view, None, None, f.quad, fs, plan["kx"], plan["ky"], g.halo,
+                                   psi_out=bufs[(k + 1) % 2], out_halo=g.halo,
+                                   delta=delta if k == 0 else None, delta_halo=0,
+                                   beta=cfg.beta_diag, sigma=self.sigma[0], qt=qt,
+                                   per_dof=per_dof, consts=c0)
+                self._t1("pg_sweep", t)
+            view.data = bufs[plan["pg_sweeps"] % 2]
+        else:
+            _lib.call("csn_sub_interior", dt, self.geoms[0], _lib.ptr(psi_in), g.halo,
+                      _lib.ptr(delta), 0, _lib.stream())
+        t = self._t0()
+        apply_boundary(view, f.quad)
+        self._t1("boundary", t)
+
+    def _commit(self, plan, psi, pg_state):
+        """Host bookkeeping after the launches: ping-pong buffer ownership."""
+        if plan["pg_sweeps"] % 2 == 1:
+            psi.data, self.psi_alt = plan["alt"], plan["psi"]
+        if plan.get("swap_avg"):
+            pg_state._avg, pg_state._avg_spare = pg_state._avg_spare, pg_state._avg
 
 
 def sawtooth_cycle(psi, q, hierarchy, fs=None, cfg=None, scheme="pg", n_sweeps=3, pg_sweeps=1,
