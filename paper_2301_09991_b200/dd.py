@@ -1,0 +1,348 @@
+"""Spatial domain decomposition: x-slabs across ranks.
+
+Rank r owns x in [X0_r, X1_r) of the global nx x ny grid on every *distributed*
+level; x is the slowest storage axis, so a slab and each of its halo bands are one
+contiguous block (no packing).  Per cycle (PG scheme):
+
+* psi ghost rows (width 3l) are refreshed before the diffusivities / residual, the
+  averaged iterate's ghost rows before a live diffusivity refresh (R/multigrid.py:282-288);
+* the residual's L1 (PGState input, R/multigrid.py:292) is an fp64 all-reduce;
+* the correction restricts locally, refreshes each level's source ghosts (3 columns:
+  the smoother's upwind warm-up), gathers the level-Lg source onto every rank,
+  solves the coarse levels Lg..L-1 redundantly (they are < ~1% of the DOF), and
+  smooths back up the distributed levels with the coarse correction's ghost columns
+  (R/multigrid.py:309-339);
+* the fused sweep reads delta's ghost rows (width l) (R/multigrid.py:301-304).
+
+Kernels are unchanged: every launch carries ``ghost_w/ghost_e`` in its geometry, so
+ghost sides read halo memory where physical sides apply the vacuum rule.
+
+Communicators: ``TorchDistComm`` (one process per GPU, ``torch.distributed`` —
+NCCL over NVLink, or gloo on CPU for tests) and ``ThreadComm`` (several ranks as
+threads of one process on one device — used to verify the decomposition against
+the single-domain solve on a single GPU).
+"""
+
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+from .eigen import Solver, SolverOptions, TransportSetup, setup_transport, _buffers
+from .filters import build_upwind_filters
+from .grid import GridSpec
+from .materials import MaterialField
+from .multigrid import (CycleEngine, Level, MultigridHierarchy, UP_MAX_SWEEPS, _smooth_chain,
+                        build_hierarchy, coarsen_sigma, max_levels)
+from .quadrature import coarsen_quadrature
+
+GX = 5   # x-ghost columns of sources / corrections: the smoother's 3-sweep warm-up and
+         # the fused sweep's l-wide read of delta (l <= 5)
+
+
+# ----------------------------------------------------------------------------- comms
+class SlabComm:
+    """Neighbour halo exchange along x + the two collectives the solver needs."""
+
+    rank = 0
+    size = 1
+
+    def exchange(self, t, width, hx):
+        """t: dim 0 = x with interior rows [hx, t.shape[0] - hx); fill `width` ghost
+        rows on each side that has a neighbour from the neighbour's interior edge."""
+        raise NotImplementedError
+
+    def allreduce_sum_(self, t):
+        raise NotImplementedError
+
+    def allgather_x(self, t):
+        """Concatenate every rank's t along dim 0 (rank order)."""
+        raise NotImplementedError
+
+
+def _edges(t, width, hx):
+    nx = t.shape[0] - 2 * hx
+    return (t[hx:hx + width], t[hx + nx - width:hx + nx],       # west / east interior edge
+            t[hx - width:hx], t[hx + nx:hx + nx + width])       # west / east ghost rows
+
+
+class TorchDistComm(SlabComm):
+    """torch.distributed (NCCL on GPUs, gloo on CPU); ranks ordered along x."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def exchange(self, t, width, hx):
+        if self.size == 1 or width == 0:
+            return
+        dist = self.dist
+        we, ee, wg, eg = _edges(t, width, hx)
+        ops, recv = [], []
+        if self.rank > 0:
+            buf = torch.empty_like(wg)
+            ops += [dist.P2POp(dist.isend, we.contiguous(), self.rank - 1, self.group),
+                    dist.P2POp(dist.irecv, buf, self.rank - 1, self.group)]
+            recv.append((wg, buf))
+        if self.rank < self.size - 1:
+            buf = torch.empty_like(eg)
+            ops += [dist.P2POp(dist.isend, ee.contiguous(), self.rank + 1, self.group),
+                    dist.P2POp(dist.irecv, buf, self.rank + 1, self.group)]
+            recv.append((eg, buf))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        for dst, buf in recv:
+            dst.copy_(buf)
+
+    def allreduce_sum_(self, t):
+        if self.size > 1:
+            self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def allgather_x(self, t):
+        if self.size == 1:
+            return t
+        parts = [torch.empty_like(t) for _ in range(self.size)]
+        self.dist.all_gather(parts, t.contiguous(), group=self.group)
+        return torch.cat(parts, dim=0)
+
+
+class _Hub:
+    def __init__(self, size):
+        self.size = size
+        self.barrier = threading.Barrier(size)
+        self.slots = {}
+
+
+class ThreadComm(SlabComm):
+    """Ranks as threads of one process sharing one device (emulation / verification).
+
+    Device copies are issued after a barrier on the (shared) default stream, so they
+    are ordered after every rank's producing kernels and before any consumer."""
+
+    def __init__(self, hub, rank):
+        self.hub = hub
+        self.rank = rank
+        self.size = hub.size
+
+    @staticmethod
+    def make(size):
+        hub = _Hub(size)
+        return [ThreadComm(hub, r) for r in range(size)]
+
+    def _post(self, key, t):
+        self.hub.slots[(key, self.rank)] = t
+        self.hub.barrier.wait()
+
+    def _done(self):
+        self.hub.barrier.wait()
+
+    def exchange(self, t, width, hx):
+        if self.size == 1 or width == 0:
+            return
+        self._post("x", t)
+        if self.rank > 0:
+            nb = self.hub.slots[("x", self.rank - 1)]
+            _edges(t, width, hx)[2].copy_(_edges(nb, width, hx)[1])
+        if self.rank < self.size - 1:
+            nb = self.hub.slots[("x", self.rank + 1)]
+            _edges(t, width, hx)[3].copy_(_edges(nb, width, hx)[0])
+        self._done()
+
+    def allreduce_sum_(self, t):
+        if self.size == 1:
+            return t
+        self._post("r", t.clone())
+        total = self.hub.slots[("r", 0)].clone()
+        for r in range(1, self.size):
+            total += self.hub.slots[("r", r)]
+        self._done()
+        t.copy_(total)
+        return t
+
+    def allgather_x(self, t):
+        if self.size == 1:
+            return t
+        self._post("g", t)
+        out = torch.cat([self.hub.slots[("g", r)] for r in range(self.size)], dim=0)
+        self._done()
+        return out
+
+
+# ----------------------------------------------------------------------------- layout
+def slab_bounds(nx, size, rank):
+    if nx % size:
+        raise ValueError(f"nx = {nx} is not divisible by {size} ranks")
+    w = nx // size
+    return rank * w, (rank + 1) * w
+
+
+def distributed_levels(nx, ny, size, n_levels):
+    """Levels that stay x-slab distributed: 2x2 blocks must not straddle ranks and each
+    slab keeps >= 2 GX columns; the rest is gathered (>= 1 level is always gathered)."""
+    w = nx // size
+    lg = 0
+    while lg < n_levels - 1 and (w >> lg) >= 2 * GX and (w >> lg) % 2 == 0:
+        lg += 1
+    return max(lg, 1)
+
+
+class _XGhost:
+    """A [nx + 2 GX, ...] tensor whose interior view starts at x = 0."""
+
+    def __init__(self, shape, dtype, device, gx=GX):
+        self.gx = gx
+        self.full = torch.zeros((shape[0] + 2 * gx,) + tuple(shape[1:]), dtype=dtype, device=device)
+        self.view = self.full[gx:gx + shape[0]]
+
+
+# ----------------------------------------------------------------------------- engine
+class DDCycleEngine(CycleEngine):
+    """CycleEngine on one rank's slab with halo exchange, L1 all-reduce and a gathered,
+    redundantly solved coarse hierarchy."""
+
+    def __init__(self, local_h, coarse_h, comm, n_group, dtype, device, sigma_ghosted,
+                 x0_levels, lg):
+        self.comm = comm
+        self.coarse_h = coarse_h
+        self.lg = lg
+        self.x0_levels = x0_levels
+        super().__init__(local_h, n_group, dtype, device)
+        west, east = comm.rank > 0, comm.rank < comm.size - 1
+        self.geoms = [lev.geom(n_group, int(west), int(east)) for lev in local_h.levels]
+        self.sigma = sigma_ghosted
+        # x-ghosted sources / corrections of the distributed levels
+        self.src_g = [_XGhost(s, dtype, device) for s in self.shapes]
+        self.delta_g = [_XGhost(s, dtype, device) for s in self.shapes]
+        self.r0 = self.src_g[0].view
+        self.src = [g.view for g in self.src_g]
+        self.delta = [g.view for g in self.delta_g]
+        self.use_graphs = False      # host barriers / NCCL calls between launches
+        cl = coarse_h.levels[0]
+        self.coarse_eng = coarse_h.engine(n_group, dtype, device)
+        self.coarse_init = _XGhost((cl.grid.nx // comm.size, cl.grid.ny, cl.quad.n_dir, n_group),
+                                   dtype, device)
+        self.coarse_geom = cl.geom(n_group, int(west), int(east))
+        cgc = cl.grid
+        self.coarse_geom.nx = cgc.nx // comm.size
+
+    def _hook_exchange(self, name, t, width):
+        h = self.h.levels[0].grid.halo
+        self.comm.exchange(t, width, h)
+
+    def _hook_l1(self):
+        self.comm.allreduce_sum_(self.l1)
+
+    def correction(self, r0, n_sweeps, finest_scale):
+        if n_sweeps > UP_MAX_SWEEPS:
+            raise ValueError("domain decomposition supports <= 3 Jacobi sweeps per level")
+        L = self.h.levels
+        dt = _lib.dtype_code(r0)
+        comm = self.comm
+        # local restriction down the distributed levels; ghosts for the smoother warm-up
+        comm.exchange(self.src_g[0].full, GX, GX)
+        for i in range(1, len(L)):
+            _lib.call("csn_restrict", dt, self.geoms[i - 1], self.geoms[i],
+                      _lib.ptr(self.src[i - 1]), 0, _lib.ptr(self.consts[i - 1]["w"]),
+                      _lib.ptr(self.consts[i]["w"]), 1, _lib.ptr(self.src[i]), 0, _lib.stream())
+            comm.exchange(self.src_g[i].full, GX, GX)
+        # gathered coarse hierarchy: restrict the last distributed level onto the coarse
+        # level's slab, gather, solve redundantly
+        cl = self.coarse_h.levels[0]
+        local_coarse = torch.empty((cl.grid.nx // comm.size,) + tuple(self.coarse_eng.shapes[0][1:]),
+                                   dtype=r0.dtype, device=r0.device)
+        _lib.call("csn_restrict", dt, self.geoms[-1], self.coarse_geom, _lib.ptr(self.src[-1]), 0,
+                  _lib.ptr(self.consts[-1]["w"]),
+                  _lib.ptr(cl.consts(r0.dtype, r0.device)["w"]), 1, _lib.ptr(local_coarse), 0,
+                  _lib.stream())
+        full = comm.allgather_x(local_coarse)
+        dc = self.coarse_eng.correction(full, n_sweeps, 1.0)
+        w = cl.grid.nx // comm.size
+        x0 = comm.rank * w
+        ci = self.coarse_init
+        ci.full.zero_()
+        lo, hi = max(x0 - GX, 0), min(x0 + w + GX, cl.grid.nx)
+        ci.full[lo - (x0 - GX):hi - (x0 - GX)].copy_(dc[lo:hi])
+        prev, gc = ci.view, self.coarse_geom
+        for i in range(len(L) - 1, -1, -1):
+            scale = finest_scale if i == 0 else 1.0
+            prev = _smooth_chain(L[i], self.ng, self.src[i], 1, prev, 2, 0, gc, n_sweeps, scale,
+                                 self.delta[i], 0, None, self.sigma[i], self.geoms[i])
+            comm.exchange(self.delta_g[i].full, GX, GX)
+            gc = self.geoms[i]
+        return prev
+
+
+def _slab_material(mf, x0, x1):
+    return MaterialField(mf.sigma_t[x0:x1].copy(), mf.sigma_s[x0:x1].copy(),
+                         mf.nu_sigma_f[x0:x1].copy(), mf.sigma_f[x0:x1].copy(),
+                         mf.chi[x0:x1].copy(), mf.source[x0:x1].copy())
+
+
+class DDSolver(Solver):
+    """Solver on one rank's x-slab; results (phi, histories, k) are global on every rank."""
+
+    def __init__(self, problem, options=None, inner_iters=None, comm=None, device=None):
+        options = options or SolverOptions()
+        comm = comm or TorchDistComm()
+        self.comm = comm
+        gsetup = setup_transport(problem, options)        # global setup (host only)
+        gh = gsetup.hierarchy
+        nl = gh.n_levels
+        lg = distributed_levels(gsetup.grid.nx, gsetup.grid.ny, comm.size, nl)
+        if lg >= nl:
+            raise ValueError("hierarchy too shallow to decompose")
+        x0, x1 = slab_bounds(gsetup.grid.nx, comm.size, comm.rank)
+        for l in range(lg + 1):   # every distributed level and the gather level split evenly
+            if (gsetup.grid.nx >> l) % comm.size:
+                raise ValueError(f"level {l} extent not divisible by {comm.size} ranks")
+        if device is not None:
+            torch.cuda.set_device(device)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        dtype = options.torch_dtype()
+        # local distributed levels 0..lg-1 and per-level x-ghosted sigma
+        levels, sig_g, x0s = [], [], []
+        for l in range(lg):
+            gl = gh.levels[l]
+            w = gl.grid.nx // comm.size
+            a0 = comm.rank * w
+            grid = GridSpec(w, gl.grid.ny, gl.grid.dx, gl.grid.dy, gl.grid.halo)
+            levels.append(Level(grid, gl.quad, gl.sigma_t[a0:a0 + w].copy(),
+                                build_upwind_filters(gl.grid.dx, gl.grid.dy)))
+            sg = _XGhost((w, gl.grid.ny, gl.sigma_t.shape[2]), dtype, dev)
+            lo, hi = max(a0 - GX, 0), min(a0 + w + GX, gl.grid.nx)
+            sg.full[lo - (a0 - GX):hi - (a0 - GX)].copy_(
+                torch.as_tensor(gl.sigma_t[lo:hi], dtype=dtype))
+            sig_g.append(sg.view)
+            x0s.append(a0)
+        local_h = MultigridHierarchy(levels)
+        coarse_h = MultigridHierarchy(gh.levels[lg:])
+        mat = _slab_material(gsetup.mat, x0, x1)
+        setup = TransportSetup(grid=levels[0].grid, quad=gsetup.quad, filters=gsetup.filters,
+                               mat=mat, hierarchy=local_h, options=options)
+        ng = mat.n_groups
+        eng = DDCycleEngine(local_h, coarse_h, comm, ng, dtype, dev, sig_g, x0s, lg)
+        local_h._engines[(ng, dtype, str(dev))] = eng
+        self.global_setup = gsetup
+        self.fissile_global = gsetup.mat.fissile
+        self.source_any = bool(gsetup.mat.source.any())
+        super().__init__(problem, options, inner_iters, setup=setup)
+
+    # global decisions must not depend on the slab's own material
+    def _production(self):
+        from .eigen import _production_dev
+        b = self.bufs
+        _production_dev(b.phi, self.setup.mat, self.setup.grid.dx, self.setup.grid.dy, b.prod,
+                        b.partials)
+        self.comm.allreduce_sum_(b.prod)
+        return float(b.prod.item())
+
+    def result(self):
+        res = super().result()
+        res.phi = self.comm.allgather_x(torch.as_tensor(res.phi, device=self.bufs.phi.device)
+                                        ).cpu().numpy()
+        return res

@@ -103,14 +103,15 @@ def _check_order(fs, halo):
 
 
 def diffusivities_into(psi_data, grid, n_dir, n_group, n_a, fs, cfg, mu, nu, kx, ky, k_halo,
-                       avg_in=None, avg_out=None, avg_mode=0, theta=1.0, psi_halo=None):
+                       avg_in=None, avg_out=None, avg_mode=0, theta=1.0, psi_halo=None, gm=None):
     """Launch the fused averaging + k kernel (K2)."""
     taps_arr = fs.taps()
     cfg_arr = cfg.host_cfg(fs.order)
     taps_p = taps_arr.ctypes.data_as(_lib._DP)
     cfg_p = cfg_arr.ctypes.data_as(_lib._DP)
     h = grid.halo if psi_halo is None else psi_halo
-    gm = _lib.geom(grid.nx, grid.ny, n_dir, n_group, n_a, fs.dx, fs.dy)
+    if gm is None:
+        gm = _lib.geom(grid.nx, grid.ny, n_dir, n_group, n_a, fs.dx, fs.dy)
     _lib.call("csn_pg_diffusivities", _lib.dtype_code(psi_data), fs.order, gm, taps_p, cfg_p,
               _lib.ptr(psi_data), h, _lib.ptr(avg_in), h, _lib.ptr(avg_out), h, avg_mode,
               float(theta), _lib.ptr(mu), _lib.ptr(nu), _lib.ptr(kx), _lib.ptr(ky), k_halo,
@@ -165,7 +166,7 @@ def pg_residual(psi, mat, q, quad, fs, cfg, diffusivities=None, anisotropy="xy")
 def pg_residual_launch(psi, mat, q, quad, fs, kx, ky, k_halo, r=None, r_halo=0, psi_out=None,
                        out_halo=0, delta=None, delta_halo=0, beta=1.0, partials=None, l1=None,
                        sigma=None, qt=None, per_dof=None, consts=None, avg=None, avg_mode=0,
-                       theta=1.0):
+                       theta=1.0, gm=None):
     d = psi.data
     g = psi.grid
     if sigma is None:
@@ -174,7 +175,8 @@ def pg_residual_launch(psi, mat, q, quad, fs, kx, ky, k_halo, r=None, r_halo=0, 
         qt, per_dof = source_tensor(q, g.nx, g.ny, psi.n_dir, psi.n_group, d)
     qd = consts or quad.device(d.dtype, d.device, fs.dx, fs.dy)
     taps_p = fs.taps().ctypes.data_as(_lib._DP)
-    gm = _lib.geom(g.nx, g.ny, psi.n_dir, psi.n_group, quad.n_a, fs.dx, fs.dy)
+    if gm is None:
+        gm = _lib.geom(g.nx, g.ny, psi.n_dir, psi.n_group, quad.n_a, fs.dx, fs.dy)
     _lib.call("csn_pg_residual", _lib.dtype_code(d), fs.order, gm, taps_p, _lib.ptr(d), g.halo,
               _lib.ptr(delta), delta_halo, _lib.ptr(kx), _lib.ptr(ky), k_halo, _lib.ptr(sigma),
               _lib.ptr(qt), per_dof, _lib.ptr(qd["mu"]), _lib.ptr(qd["nu"]), _lib.ptr(qd["strm"]),

@@ -232,7 +232,8 @@ class Solver:
         self.dtype = options.torch_dtype()
         self.dev = default_device()
         mat = setup.mat
-        self.eigen = bool(mat.fissile)
+        # global properties (a domain-decomposed slab may hold no fuel / no source)
+        self.eigen = bool(getattr(self, "fissile_global", mat.fissile))
         g = setup.grid
         ng = mat.n_groups
         self.psi = Field(g, setup.quad.n_dir, ng, dtype=self.dtype, device=self.dev)
@@ -259,7 +260,7 @@ class Solver:
             _scale(self.bufs.phi, prod)
             self.phases = [("boot", n_boot)] + [("outer", self.inner)] * options.outer_iters
         else:
-            self.empty = not mat.source.any()
+            self.empty = not getattr(self, "source_any", bool(mat.source.any()))
             self.phases = [] if self.empty else [("boot", n_boot), ("main", options.mg_iters)]
         self.phases = [ph for ph in self.phases if ph[1] > 0]
         self.phase = 0

@@ -176,12 +176,14 @@ def prolong(field, coarse_level, fine_level):
 
 
 def _smooth_chain(level, ng, src, per_dof, init, init_mode, init_halo, gc, n_sweeps, scale,
-                  out, out_halo, spare):
+                  out, out_halo, spare, sig=None, g=None):
     """Run n_sweeps upwind sweeps in launches of <= 3 (ping-pong through `spare`)."""
     d = out
     c = level.consts(d.dtype, d.device)
-    sig = level.sigma_dev(d.dtype, d.device)
-    g = level.geom(ng)
+    if sig is None:
+        sig = level.sigma_dev(d.dtype, d.device)
+    if g is None:
+        g = level.geom(ng)
     dt = _lib.dtype_code(d)
     first = min(n_sweeps, UP_MAX_SWEEPS)
     bufs = [out, spare]
@@ -419,8 +421,15 @@ class CycleEngine:
             else:
                 init, mode, gc = prev, 2, self.geoms[i + 1]
             prev = _smooth_chain(L[i], self.ng, src[i], 1, init, mode, 0, gc, n_sweeps, scale,
-                                 self.delta[i], 0, self.spare[i])
+                                 self.delta[i], 0, self.spare[i], self.sigma[i], self.geoms[i])
         return prev
+
+    # hooks for domain decomposition (dd.py): halo exchange / reductions; no-ops here
+    def _hook_exchange(self, name, t, width):
+        pass
+
+    def _hook_l1(self):
+        pass
 
     # ---------------------------------------------------------------- cycle
     def cycle(self, psi, q, fs=None, cfg=None, scheme="pg", n_sweeps=3, pg_sweeps=1,
@@ -546,21 +555,25 @@ class CycleEngine:
         view.grid = g
         view.data = psi_in
         nd, ng, na = psi_in.shape[2], psi_in.shape[3], f.quad.n_a
+        reach = 3 * fs.half_width if scheme == "pg" else 1
+        self._hook_exchange("psi", psi_in, reach)
         if scheme == "pg":
             kx, ky = plan["kx"], plan["ky"]
             if plan["k2"] is not None:
                 avg_in, avg_out, mode, theta = plan["k2"]
+                if avg_in is not None:
+                    self._hook_exchange("avg", avg_in, reach)
                 t = self._t0()
                 diffusivities_into(psi_in, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky,
                                    g.halo, avg_in=avg_in, avg_out=avg_out, avg_mode=mode,
-                                   theta=theta)
+                                   theta=theta, gm=self.geoms[0])
                 self._t1("pg_diffusivity", t)
             ema = plan["ema"]
             t = self._t0()
             pg_residual_launch(view, None, None, f.quad, fs, kx, ky, g.halo, r=self.r0, r_halo=0,
                                partials=self.partials, l1=self.l1, sigma=self.sigma[0], qt=qt,
                                per_dof=per_dof, consts=c0, avg=ema[0], avg_mode=ema[1],
-                               theta=ema[2])
+                               theta=ema[2], gm=self.geoms[0])
             self._t1("pg_residual" if ema[1] == 0 else "pg_residual+ema", t)
         else:
             t = self._t0()
@@ -569,6 +582,7 @@ class CycleEngine:
                       _lib.ptr(c0["nu"]), _lib.ptr(self.r0), 0, _lib.ptr(self.partials),
                       _lib.ptr(self.l1), _lib.stream())
             self._t1("upwind_residual", t)
+        self._hook_l1()
         self.res_host.copy_(self.l1, non_blocking=True)
         t = self._t0()
         delta = self.correction(self.r0, n_sweeps, cfg.beta_diag if scheme == "pg" else 1.0)
@@ -582,14 +596,15 @@ class CycleEngine:
                                    psi_out=bufs[(k + 1) % 2], out_halo=g.halo,
                                    delta=delta if k == 0 else None, delta_halo=0,
                                    beta=cfg.beta_diag, sigma=self.sigma[0], qt=qt,
-                                   per_dof=per_dof, consts=c0)
+                                   per_dof=per_dof, consts=c0, gm=self.geoms[0])
                 self._t1("pg_sweep", t)
             view.data = bufs[plan["pg_sweeps"] % 2]
         else:
             _lib.call("csn_sub_interior", dt, self.geoms[0], _lib.ptr(psi_in), g.halo,
                       _lib.ptr(delta), 0, _lib.stream())
         t = self._t0()
-        apply_boundary(view, f.quad)
+        _lib.call("csn_apply_boundary", dt, self.geoms[0], _lib.ptr(view.data), g.halo,
+                  _lib.ptr(c0["mu"]), _lib.ptr(c0["nu"]), _lib.stream())
         self._t1("boundary", t)
 
     def _commit(self, plan, psi, pg_state):
