@@ -171,6 +171,18 @@ int csn_sub_interior(int dtype, const csn_geom* g, void* psi, int psi_halo,
 int csn_ema(int dtype, const csn_geom* g, void* avg, int avg_halo, const void* psi,
             int psi_halo, double theta, int mode, void* stream);
 
+/* Non-default PG modes (R/discretisation.py:164-224), elementwise over n elements of
+ * same-layout arrays with C channels per cell, ng groups (ordinate = (e % C) / ng):
+ *   csn_dir_lincomb:     out = scale (ca A[n] x + cb B[n] y)   (A, B, y nullable);
+ *   csn_iso_diffusivity: isotropic k from the residual estimate r and psi_x, psi_y,
+ *                        cfg = {epsilon_k, alpha_kabs, alpha_ksquare, (dx+dy)/2, dx, dy}. */
+int csn_dir_lincomb(int dtype, int64_t n, int C, int ng, const void* x, const void* A, double ca,
+                    const void* y, const void* B, double cb, double scale, void* out,
+                    void* stream);
+int csn_iso_diffusivity(int dtype, int64_t n, int C, int ng, const void* r, const void* px,
+                        const void* py, const void* mu, const void* nu, const double* cfg,
+                        void* k, void* stream);
+
 /* R/grid.py:85-105,139-152 convolve: square (2l+1)^2 stencil, host `stencil`
  * [width][width] (fp64), on interior +- margin, reading halo memory as stored;
  * dir_scale: device [nd] or NULL.  Writes the whole padded `out` (0 outside). */

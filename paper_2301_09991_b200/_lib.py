@@ -54,6 +54,10 @@ _SIGNATURES = {
     "csn_scale": ([_c_int, _vp, _c_i64, _c_dbl, _c_int, _vp], _c_int),
     "csn_sub_interior": ([_c_int, _GP, _vp, _c_int, _vp, _c_int, _vp], _c_int),
     "csn_ema": ([_c_int, _GP, _vp, _c_int, _vp, _c_int, _c_dbl, _c_int, _vp], _c_int),
+    "csn_dir_lincomb": ([_c_int, _c_i64, _c_int, _c_int, _vp, _vp, _c_dbl, _vp, _vp, _c_dbl, _c_dbl,
+                         _vp, _vp], _c_int),
+    "csn_iso_diffusivity": ([_c_int, _c_i64, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _DP, _vp,
+                             _vp], _c_int),
     "csn_convolve": ([_c_int, _GP, _vp, _c_int, _DP, _c_int, _c_int, _vp, _vp, _vp], _c_int),
     "csn_pass1d": ([_c_int, _GP, _vp, _c_int, _DP, _c_int, _c_int, _c_int, _vp, _vp], _c_int),
 }

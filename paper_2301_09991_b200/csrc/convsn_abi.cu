@@ -511,6 +511,34 @@ int csn_ema(int dtype, const csn_geom* g, void* avg, int avg_halo, const void* p
     return CSN_OK;
 }
 
+int csn_dir_lincomb(int dtype, int64_t n, int C, int ng, const void* x, const void* A, double ca,
+                    const void* y, const void* B, double cb, double scale, void* out,
+                    void* stream) {
+    if (!x || !out || n < 0 || C < 1 || ng < 1) return CSN_E_ARG;
+    if (n == 0) return CSN_OK;
+    if (dtype == CSN_F32)
+        dir_lincomb_kernel<float><<<grid1d(n), 256, 0, S(stream)>>>(n, C, ng, (const float*)x, (const float*)A, (float)ca, (const float*)y, (const float*)B, (float)cb, (float)scale, (float*)out);
+    else if (dtype == CSN_F64)
+        dir_lincomb_kernel<double><<<grid1d(n), 256, 0, S(stream)>>>(n, C, ng, (const double*)x, (const double*)A, ca, (const double*)y, (const double*)B, cb, scale, (double*)out);
+    else return CSN_E_DTYPE;
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
+int csn_iso_diffusivity(int dtype, int64_t n, int C, int ng, const void* r, const void* px,
+                        const void* py, const void* mu, const void* nu, const double* cfg,
+                        void* k, void* stream) {
+    if (!r || !px || !py || !mu || !nu || !cfg || !k || n < 0) return CSN_E_ARG;
+    if (n == 0) return CSN_OK;
+    if (dtype == CSN_F32)
+        iso_diffusivity_kernel<float><<<grid1d(n), 256, 0, S(stream)>>>(n, C, ng, (const float*)r, (const float*)px, (const float*)py, (const float*)mu, (const float*)nu, (float)cfg[0], (float)cfg[1], (float)cfg[2], (float)cfg[3], (float)cfg[4], (float)cfg[5], (float*)k);
+    else if (dtype == CSN_F64)
+        iso_diffusivity_kernel<double><<<grid1d(n), 256, 0, S(stream)>>>(n, C, ng, (const double*)r, (const double*)px, (const double*)py, (const double*)mu, (const double*)nu, cfg[0], cfg[1], cfg[2], cfg[3], cfg[4], cfg[5], (double*)k);
+    else return CSN_E_DTYPE;
+    CSN_CHECK_LAUNCH();
+    return CSN_OK;
+}
+
 int csn_convolve(int dtype, const csn_geom* g, const void* src, int halo, const double* stencil,
                  int width, int margin, const void* dir_scale, void* out, void* stream) {
     if (!geom_ok(g) || !src || !stencil || !out || width < 1 || width > 11 || !(width & 1))

@@ -246,6 +246,41 @@ ema_kernel(Geo g, Real* avg, int ah, const Real* psi, int ph, Real theta, Real o
     }
 }
 
+// ------------------------------------------------------------------ elementwise (modes)
+// out = s (ca A[n] x + cb B[n] y); A/B per-ordinate coefficients or null (= 1)
+template <class Real>
+__global__ void __launch_bounds__(256)
+dir_lincomb_kernel(int64_t n, int C, int ng, const Real* x, const Real* A, Real ca, const Real* y,
+                   const Real* B, Real cb, Real scale, Real* out) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int d = (int)(e % C) / ng;
+        const Real a = A ? A[d] * x[e] : x[e];
+        const Real b = y ? (B ? B[d] * y[e] : y[e]) : Real(0);
+        out[e] = scale * (ca * a + cb * b);
+    }
+}
+
+// isotropic PG diffusivity (R/discretisation.py:164-185), elementwise
+template <class Real>
+__global__ void __launch_bounds__(256)
+iso_diffusivity_kernel(int64_t n, int C, int ng, const Real* r, const Real* px, const Real* py,
+                       const Real* mu, const Real* nu, Real eps, Real a_abs, Real a_sq, Real hh,
+                       Real dx, Real dy, Real* k) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int d = (int)(e % C) / ng;
+        const Real m = mu[d], v = nu[d];
+        const Real rx = r[e], gx = px[e], gy = py[e];
+        const Real k_abs = a_abs * fabs(rx) * hh / (eps + Real(0.5) * (fabs(gx) + fabs(gy)));
+        const Real ratio = (m * gx + v * gy) / (eps + gx * gx + gy * gy);
+        const Real k_sq = a_sq * (rx * rx) * hh /
+                          (eps + Real(0.5) * (fabs(ratio * gx) + fabs(ratio * gy)) * (gx * gx + gy * gy));
+        const Real k_max = sqrt((dx * m) * (dx * m) + (dy * v) * (dy * v));
+        k[e] = nanmin(k_max, nanmin(k_abs, k_sq));
+    }
+}
+
 // ------------------------------------------------------------------ generic stencils
 // R/grid.py:85-105: out = scale[n] * sum_{a,b} w[a][b] src[i+a-l][j+b-l] on
 // interior +- margin; whole padded output written (zeros elsewhere).

@@ -119,6 +119,17 @@ def test_pg_operators(P, p, dt, tol):
     P.jacobi_sweep(sw, g["qcell"], lev, n_sweeps=1, scheme="pg", cfg=cfg, fs=fs,
                    diffusivities=(kx, ky))
     assert rel_l2(interior(host(sw.data), h), interior(g[f"pg{p}_sweep"], h)) < tol
+    # non-default modes: isotropic diffusivity and the residual-estimate variants
+    r_iso = P.pg_residual(psi, g["sigma"], g["qcell"], q, fs, cfg, anisotropy="iso")
+    assert rel_l2(host(r_iso.data), g[f"pg{p}_r_iso"]) < tol * 10
+    for mode, key in (("mixed_mass", "alt_mixed"), ("high_order", "alt_high"),
+                      ("low_order", "alt_low")):
+        if mode == "low_order" and p < 2:
+            with pytest.raises(ValueError):
+                P.residual_alternatives(psi, fs, q, cfg, mode)
+            continue
+        alt = P.residual_alternatives(psi, fs, q, cfg, mode)
+        assert rel_l2(interior(host(alt.data), h), interior(g[f"pg{p}_{key}"], h)) < tol * 10
 
 
 @pytest.mark.parametrize("na,ng", [(4, 2), (1, 1), (2, 3)])
