@@ -322,10 +322,27 @@ def make_drivers(full=True):
         run_driver(B.c2(), "c2_full")
 
 
+def make_krylov():
+    """R/krylov.py:54-104 on two tiny problems (bootstrap + frozen-k Picard/GMRES)."""
+    from convsn import krylov as rk
+    out = {}
+    for tag, pd, kw in (("q", B.c2(nx=16, blocks=4, n_a=1, cycles=1), dict(picard_iters=3)),
+                        ("l", B.c2(nx=16, blocks=2, n_a=2, cycles=1), dict(picard_iters=2))):
+        pd.options.update(order=2 if tag == "q" else 1, bootstrap_cycles=3)
+        t0 = time.perf_counter()
+        res = rk.solve_fixed_source_krylov(ref_problem(pd), ref_options(pd), **kw)
+        out[f"{tag}_phi"] = res.phi
+        out[f"{tag}_hist"] = np.array(res.residual_history)
+        out[f"{tag}_converged"] = np.array(res.converged)
+        print(tag, "krylov", time.perf_counter() - t0, "s", res.residual_history, res.converged)
+    save("krylov", **out)
+
+
 if __name__ == "__main__":
     what = sys.argv[1:] or ["setup", "ops", "transfer", "cycles", "drivers"]
     for w in what:
         {"setup": make_setup, "ops": make_ops, "transfer": make_transfer,
          "cycles": make_cycles, "drivers": make_drivers,
          "drivers_small": lambda: make_drivers(False),
-         "c2full": lambda: run_driver(B.c2(), "c2_full")}[w]()
+         "c2full": lambda: run_driver(B.c2(), "c2_full"),
+         "krylov": make_krylov}[w]()

@@ -257,3 +257,19 @@ def test_dense_known_answer(P):
         st = P.power_iteration(prob, P.SolverOptions(scheme="upwind", n_a=1, mg_iters=25,
                                                      outer_iters=200, dtype=dtype))
         assert abs(st.k_eff - 2.79519174) < tol
+
+
+@pytest.mark.parametrize("tag,order,blocks,na,picard", [("q", 2, 4, 1, 3), ("l", 1, 2, 2, 2)])
+def test_krylov_driver(P, tag, order, blocks, na, picard):
+    """R/krylov.py:54-104: frozen-k Picard + left-preconditioned GMRES (fp64)."""
+    from paper_2301_09991_b200 import benchmarks as B
+    from paper_2301_09991_b200.krylov import solve_fixed_source_krylov
+    from paper_2301_09991_b200.problems import problem_from_data
+    g = golden("krylov")
+    pd = B.c2(nx=16, blocks=blocks, n_a=na, cycles=1)
+    opts = P.SolverOptions(scheme="pg", order=order, n_a=na, mg_iters=1, bootstrap_cycles=3,
+                           dtype="float64")
+    res = solve_fixed_source_krylov(problem_from_data(pd), opts, picard_iters=picard)
+    assert rel_l2(res.phi, g[f"{tag}_phi"]) < 1e-7
+    np.testing.assert_allclose(res.residual_history, g[f"{tag}_hist"], rtol=1e-6)
+    assert res.converged == bool(g[f"{tag}_converged"])
