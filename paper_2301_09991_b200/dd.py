@@ -336,8 +336,8 @@ class DDSolver(Solver):
     def _production(self):
         from .eigen import _production_dev
         b = self.bufs
-        _production_dev(b.phi, self.setup.mat, self.setup.grid.dx, self.setup.grid.dy, b.prod,
-                        b.partials)
+        _production_dev(self.phi_outer, self.setup.mat, self.setup.grid.dx, self.setup.grid.dy,
+                        b.prod, b.partials)
         self.comm.allreduce_sum_(b.prod)
         return float(b.prod.item())
 

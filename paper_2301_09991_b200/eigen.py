@@ -250,14 +250,17 @@ class Solver:
             self.inner = options.mg_iters if inner_iters is None else inner_iters
             self.md = mat.device(self.dev)
             self.gm = _lib.geom(g.nx, g.ny, 1, ng, 1, g.dx, g.dy)
+            # the power iteration's own phi (R/eigen.py:212-219,238-248): frozen-fission
+            # input of each block, separate from the per-cycle flux of the group source
+            self.phi_outer = torch.zeros_like(self.bufs.phi)
             self.psi.fill(1.0)
             apply_boundary(self.psi, setup.quad)
-            scalar_flux_into(self.psi, setup.quad, self.bufs.phi)
+            scalar_flux_into(self.psi, setup.quad, self.phi_outer)
             prod = self._production()
             if prod <= 0.0:
                 raise ValueError("initial fission production is zero")
             _scale(self.psi.data, prod)
-            _scale(self.bufs.phi, prod)
+            _scale(self.phi_outer, prod)
             self.phases = [("boot", n_boot)] + [("outer", self.inner)] * options.outer_iters
         else:
             self.empty = not getattr(self, "source_any", bool(mat.source.any()))
@@ -270,12 +273,12 @@ class Solver:
 
     # ------------------------------------------------------------------ pieces
     def _production(self):
-        _production_dev(self.bufs.phi, self.setup.mat, self.setup.grid.dx, self.setup.grid.dy,
+        _production_dev(self.phi_outer, self.setup.mat, self.setup.grid.dx, self.setup.grid.dy,
                         self.bufs.prod, self.bufs.partials)
         return float(self.bufs.prod.item())
 
     def _frozen_fission(self, inv_k):
-        _lib.call("csn_fission_source", self.gm, _lib.ptr(self.bufs.phi), _lib.ptr(self.md["chi"]),
+        _lib.call("csn_fission_source", self.gm, _lib.ptr(self.phi_outer), _lib.ptr(self.md["chi"]),
                   _lib.ptr(self.md["nu_sigma_f"]), float(inv_k), _lib.ptr(self.bufs.fission),
                   _lib.stream())
         return self.bufs.fission
@@ -333,7 +336,7 @@ class Solver:
 
     def _outer_update(self):
         """k <- k P; psi, phi, psi_avg /= P (R/eigen.py:238-248)."""
-        scalar_flux_into(self.psi, self.setup.quad, self.bufs.phi)
+        scalar_flux_into(self.psi, self.setup.quad, self.phi_outer)
         prod = self._production()
         self.outer_done += 1
         if not math.isfinite(prod) or prod <= 0.0:
@@ -341,7 +344,7 @@ class Solver:
                              f"{self.outer_done}")
         self.k = self.k * prod
         _scale(self.psi.data, prod)
-        _scale(self.bufs.phi, prod)
+        _scale(self.phi_outer, prod)
         self.pgs.scale_average(prod)
         self.k_history.append(self.k)
 
@@ -353,7 +356,7 @@ class Solver:
     def result(self):
         setup, ng = self.setup, self.setup.mat.n_groups
         if self.eigen:
-            return EigenState(psi=self.psi, phi=self.bufs.phi.cpu().numpy(), k_eff=self.k,
+            return EigenState(psi=self.psi, phi=self.phi_outer.cpu().numpy(), k_eff=self.k,
                               iteration=self.options.outer_iters, history=self.k_history,
                               residual_history=self.history, pg_log=list(self.pgs.log))
         if self.empty:

@@ -11,6 +11,7 @@ hierarchy and issues the kernel sequence; the per-cycle host work is the fp64
 residual read-back that drives ``PGState``.
 """
 
+import gc
 import numpy as np
 import torch
 
@@ -481,18 +482,27 @@ class CycleEngine:
 
     def _capture(self, run):
         """Capture `run` into a CUDA graph on a side stream (no GC / cache flush, unlike
-        torch.cuda.graph); all buffers are preallocated, nothing allocates inside."""
+        torch.cuda.graph); all buffers are preallocated, nothing allocates inside.  The
+        cyclic GC is paused instead: a collection inside the capture could destroy an
+        unreachable graph of another engine, and its pool release would invalidate this
+        capture."""
         graph = torch.cuda.CUDAGraph()
         if self._cap_stream is None:
             self._cap_stream = torch.cuda.Stream(device=self.device)
         cur = torch.cuda.current_stream()
         self._cap_stream.wait_stream(cur)
-        with torch.cuda.stream(self._cap_stream):
-            graph.capture_begin()
-            try:
-                run()
-            finally:
-                graph.capture_end()
+        gc_on = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.stream(self._cap_stream):
+                graph.capture_begin()
+                try:
+                    run()
+                finally:
+                    graph.capture_end()
+        finally:
+            if gc_on:
+                gc.enable()
         cur.wait_stream(self._cap_stream)
         return graph
 

@@ -322,6 +322,24 @@ def make_drivers(full=True):
         run_driver(B.c2(), "c2_full")
 
 
+def make_benchmarks():
+    """The reference's own two benchmarks (R/problems.py) with default bootstrap cycles."""
+    from convsn.problems import build_fuel_assembly, build_straight_duct, synthetic_xs_path
+    with ObserveLog() as log:
+        st = re.power_iteration(build_fuel_assembly(False, synthetic_xs_path(), n_pins=4),
+                                re.SolverOptions(scheme="pg", order=1, n_a=1, mg_iters=2,
+                                                 outer_iters=3), inner_iters=2)
+    save("assembly4", phi=st.phi, k_history=np.array(st.history),
+         residual_history=np.array(st.residual_history),
+         pg_log=np.array(log.events, dtype=np.int64).reshape(-1, 2))
+    with ObserveLog() as log:
+        res = re.solve_fixed_source(build_straight_duct(0.8),
+                                    re.SolverOptions(scheme="pg", order=2, n_a=1, mg_iters=6))
+    save("duct08", phi=res.phi, residual_history=np.array(res.residual_history),
+         boot=np.array(res.bootstrap_history),
+         pg_log=np.array(log.events, dtype=np.int64).reshape(-1, 2))
+
+
 def make_krylov():
     """R/krylov.py:54-104 on two tiny problems (bootstrap + frozen-k Picard/GMRES)."""
     from convsn import krylov as rk
@@ -345,4 +363,4 @@ if __name__ == "__main__":
          "cycles": make_cycles, "drivers": make_drivers,
          "drivers_small": lambda: make_drivers(False),
          "c2full": lambda: run_driver(B.c2(), "c2_full"),
-         "krylov": make_krylov}[w]()
+         "krylov": make_krylov, "benchmarks": make_benchmarks}[w]()

@@ -273,3 +273,42 @@ def test_krylov_driver(P, tag, order, blocks, na, picard):
     assert rel_l2(res.phi, g[f"{tag}_phi"]) < 1e-7
     np.testing.assert_allclose(res.residual_history, g[f"{tag}_hist"], rtol=1e-6)
     assert res.converged == bool(g[f"{tag}_converged"])
+
+
+def test_cli_and_dense_oracle(P, tmp_path):
+    """`oracle compare` (R/cli.py:180-191) and the drivers' on-disk outputs."""
+    from paper_2301_09991_b200.cli import main
+    assert main(["oracle", "compare"]) == 0
+    assert main(["oracle", "compare", "--nx", "4", "--ny", "4", "--groups", "1"]) == 0
+    out = tmp_path / "duct"
+    rc = main(["duct", "--dx", "0.8", "--na", "1", "--order", "linear", "--mg-iters", "3",
+               "--out", str(out), "--profile-x", "18"])
+    assert rc == 0
+    for name in ("flux_g1.csv", "flux.vtk", "metrics.csv", "manifest.txt", "profile_x18.csv"):
+        assert (out / name).exists()
+    out2 = tmp_path / "asm"
+    assert main(["assembly", "--pins", "4", "--na", "1", "--order", "linear", "--mg-iters", "2",
+                 "--outer-iters", "2", "--out", str(out2)]) == 0
+    assert (out2 / "keff_history.csv").read_text().count("\n") == 4
+
+
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-10), ("float32", 1e-5)])
+def test_reference_benchmarks_with_bootstrap(P, dtype, tol):
+    """The reference's fuel assembly (4x4 pins) and straight duct with the default
+    20 upwind bootstrap cycles (R/eigen.py:46-51,178-180,225-230)."""
+    g = golden("assembly4")
+    st = P.power_iteration(P.build_fuel_assembly(False, P.synthetic_xs_path(), n_pins=4),
+                           P.SolverOptions(scheme="pg", order=1, n_a=1, mg_iters=2,
+                                           outer_iters=3, dtype=dtype), inner_iters=2)
+    np.testing.assert_allclose(st.history, g["k_history"], rtol=tol)
+    assert rel_l2(st.phi, g["phi"]) < tol
+    g = golden("duct08")
+    res = P.solve_fixed_source(P.build_straight_duct(0.8),
+                               P.SolverOptions(scheme="pg", order=2, n_a=1, mg_iters=6,
+                                               dtype=dtype))
+    assert rel_l2(res.phi, g["phi"]) < tol
+    # the bootstrap L1 falls ~14 decades: compare relative to its start
+    np.testing.assert_allclose(res.bootstrap_history, g["boot"], rtol=tol * 10,
+                               atol=tol * float(g["boot"][0]))
+    h = g["residual_history"]
+    np.testing.assert_allclose(res.residual_history, h, rtol=tol * 10, atol=tol * float(h[0]))
