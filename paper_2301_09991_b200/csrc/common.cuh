@@ -72,7 +72,7 @@ __device__ __forceinline__ void cp_async_s(unsigned saddr, const void* gmem, boo
 }
 
 // Row stager of the y-marching stencil kernels.  A staged row holds up to 4 fields x
-// W cells x 32 channels (smem layout [field][cell][channel]).  An item is one
+// W cells x CC channels (smem layout [field][cell][channel]).  An item is one
 // (cell, VEC-channel group) and stages that vector of every field, so the thread
 // that owns an item can post-process it (psi - delta, the EMA) right after its own
 // copies land.  Everything row independent — shared address, x resolution of the
@@ -87,7 +87,7 @@ struct FieldDesc {
     int xlo = -(1 << 30), xhi = 1 << 30;   // stage only cells with xlo <= x < xhi
 };
 
-template <class Real, int VEC, int NI, int NF, int KMASK>
+template <class Real, int VEC, int NI, int NF, int KMASK, int CC = 32>
 struct Stager {
     const Real* base[NI][NF];   // field pointer at (x storage, y = 0), nullptr = zero in x
     unsigned soff[NI];          // shared byte offset of the item (field 0, buffer 0)
@@ -98,7 +98,7 @@ struct Stager {
     __device__ __forceinline__ void init(const Geo& g, const FieldDesc* fd, int x0, int W,
                                          int c0, int band_, const Real* mu, const Real* nu,
                                          int tid, int nthreads) {
-        constexpr int G4 = 32 / VEC;
+        constexpr int G4 = CC / VEC;
         ny = g.ny; C = g.C; band = band_;
 #pragma unroll
         for (int i = 0; i < NI; ++i) {
@@ -111,7 +111,7 @@ struct Stager {
             const int n = (cval ? c : 0) / g.ng;
             const bool mp = mu[n] > Real(0);
             npos[i] = nu[n] > Real(0);
-            soff[i] = (unsigned)((xi * 32 + q * VEC) * sizeof(Real));
+            soff[i] = (unsigned)((xi * CC + q * VEC) * sizeof(Real));
             const int xg = x0 + xi;
 #pragma unroll
             for (int f = 0; f < NF; ++f) {

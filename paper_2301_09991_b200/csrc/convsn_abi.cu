@@ -6,6 +6,7 @@
 #include "common.cuh"
 #include "misc_kernels.cuh"
 #include "pg_kernels.cuh"
+#include "pg_kernels_x2.cuh"
 #include "upwind_kernels.cuh"
 
 using namespace csn;
@@ -74,6 +75,22 @@ void launch_pg_resid(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<R
     pg_residual_kernel<Real, L, MODE, VEC><<<grid, block, sm, st>>>(a);
 }
 
+template <int L, int MODE, int VEC>
+void launch_pg_resid_x2(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<float>& a) {
+    constexpr size_t sm = pg_residual_x2_smem<L, MODE>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_residual_x2_kernel<L, MODE, VEC>, sm); attr = true; }
+    pg_residual_x2_kernel<L, MODE, VEC><<<grid, block, sm, st>>>(a);
+}
+
+template <int L, bool EMA, int VEC>
+void launch_pg_k_x2(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a) {
+    constexpr size_t sm = pg_k_x2_smem<L, EMA>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_diffusivity_x2_kernel<L, EMA, VEC>, sm); attr = true; }
+    pg_diffusivity_x2_kernel<L, EMA, VEC><<<grid, block, sm, st>>>(a);
+}
+
 template <class Real, int L, bool EMA, int VEC>
 void launch_pg_k(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<Real>& a) {
     constexpr size_t sm = pg_k_smem<Real, L, EMA>();
@@ -107,14 +124,37 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
     a.hx = (Real)(0.5 / (g->dx * g->dx)); a.hy = (Real)(0.5 / (g->dy * g->dy));
     a.r = (Real*)r; a.r_h = r_h;
     a.out = (Real*)out; a.out_h = out_h; a.beta = (Real)beta;
+    // fp32: packed-fp32x2 kernel, a lane per channel pair (64 channels per CTA)
+    constexpr bool X2 = sizeof(Real) == 4;
     const int gx = (int)cdiv(g->nx, PG_TX);
-    const int gy = (int)cdiv((int64_t)g->nd * g->ng, PG_CC);
+    const int gy = (int)cdiv((int64_t)g->nd * g->ng, X2 ? X2_CC : PG_CC);
     a.ly = pick_ly((int64_t)gx * gy, g->ny, T);
     const int gz = (int)cdiv(g->ny, a.ly);
     a.partials = (l1 || partials) ? partials : nullptr;
     dim3 grid(gx, gy, gz), block(PG_CC, PG_TX);
     const bool vec = vec_ok(g, 16 / (int)sizeof(Real));
     constexpr int V = 16 / sizeof(Real);
+    if constexpr (X2) {
+        if (out) {
+            if (vec) launch_pg_resid_x2<L, PG_SWEEP, V>(grid, block, st, a);
+            else launch_pg_resid_x2<L, PG_SWEEP, 1>(grid, block, st, a);
+        } else {
+            if (l1 && !partials) return CSN_E_ARG;
+            if (a.avg_mode) {
+                if (vec) launch_pg_resid_x2<L, PG_RESID_EMA, V>(grid, block, st, a);
+                else launch_pg_resid_x2<L, PG_RESID_EMA, 1>(grid, block, st, a);
+            } else {
+                if (vec) launch_pg_resid_x2<L, PG_RESID, V>(grid, block, st, a);
+                else launch_pg_resid_x2<L, PG_RESID, 1>(grid, block, st, a);
+            }
+        }
+        CSN_CHECK_LAUNCH();
+        if (!out && l1) {
+            sum_f64_kernel<<<1, 1024, 0, st>>>(partials, (int64_t)gx * gy * gz, 1.0, l1);
+            CSN_CHECK_LAUNCH();
+        }
+        return CSN_OK;
+    }
     if (out) {
         if (vec) launch_pg_resid<Real, L, PG_SWEEP, V>(grid, block, st, a);
         else launch_pg_resid<Real, L, PG_SWEEP, 1>(grid, block, st, a);
@@ -161,13 +201,30 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
     a.inv_dx = (Real)(1.0 / g->dx); a.inv_dy = (Real)(1.0 / g->dy);
     a.mu = (const Real*)mu; a.nu = (const Real*)nu;
     a.kx = (Real*)kx; a.ky = (Real*)ky; a.k_h = k_h;
+    constexpr int V = 16 / sizeof(Real);
+    const bool vec = vec_ok(g, V);
+    if constexpr (sizeof(Real) == 4 && L <= 3) {   // packed fp32x2, a lane per channel pair
+        constexpr int TXO2 = X2_KT - 2 * L;
+        const int gx = (int)cdiv(g->nx + 2 * L, TXO2);
+        const int gy = (int)cdiv((int64_t)g->nd * g->ng, X2_CC);
+        a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T);
+        const int gz = (int)cdiv(g->ny + 2 * L, a.ly);
+        dim3 grid(gx, gy, gz), block(32, X2_KT);
+        if (avg_mode == 2) {
+            if (vec) launch_pg_k_x2<L, true, V>(grid, block, st, a);
+            else launch_pg_k_x2<L, true, 1>(grid, block, st, a);
+        } else {
+            if (vec) launch_pg_k_x2<L, false, V>(grid, block, st, a);
+            else launch_pg_k_x2<L, false, 1>(grid, block, st, a);
+        }
+        CSN_CHECK_LAUNCH();
+        return CSN_OK;
+    }
     const int gx = (int)cdiv(g->nx + 2 * L, TXO);
     const int gy = (int)cdiv((int64_t)g->nd * g->ng, PG_CC);
     a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T);
     const int gz = (int)cdiv(g->ny + 2 * L, a.ly);
     dim3 grid(gx, gy, gz), block(PG_CC, KT);
-    constexpr int V = 16 / sizeof(Real);
-    const bool vec = vec_ok(g, V);
     if (avg_mode == 2) {
         if (vec) launch_pg_k<Real, L, true, V>(grid, block, st, a);
         else launch_pg_k<Real, L, true, 1>(grid, block, st, a);
