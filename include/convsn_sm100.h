@@ -114,7 +114,12 @@ int csn_pg_diffusivities(int dtype, int order, const csn_geom* g, const double* 
                          const void* avg_in, int avg_in_halo, void* avg_out,
                          int avg_out_halo, int avg_mode, double theta,
                          const void* mu, const void* nu, void* kx, void* ky, int k_halo,
-                         void* stream);
+                         void* work, void* stream);
+
+/* Bytes of the optional csn_pg_diffusivities workspace (0: the dtype/order has no
+ * split path).  With a workspace the fp32 kernel runs as two y-marches through
+ * psi_x, psi_y on the +-2l band (bit-identical k); work = NULL keeps the fused one. */
+int64_t csn_pg_workspace_size(int dtype, const csn_geom* g, int order);
 
 /* R/discretisation.py:227-276 pg_residual (anisotropy "xy", given diffusivities),
  * two modes:

@@ -42,7 +42,8 @@ _SIGNATURES = {
     "csn_restrict": ([_c_int, _GP, _GP, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _vp], _c_int),
     "csn_prolong": ([_c_int, _GP, _GP, _vp, _c_int, _vp, _c_int, _vp], _c_int),
     "csn_pg_diffusivities": ([_c_int, _c_int, _GP, _DP, _DP, _vp, _c_int, _vp, _c_int, _vp, _c_int,
-                              _c_int, _c_dbl, _vp, _vp, _vp, _vp, _c_int, _vp], _c_int),
+                              _c_int, _c_dbl, _vp, _vp, _vp, _vp, _c_int, _vp, _vp], _c_int),
+    "csn_pg_workspace_size": ([_c_int, _GP, _c_int], _c_i64),
     "csn_pg_residual": ([_c_int, _c_int, _GP, _DP, _vp, _c_int, _vp, _c_int, _vp, _vp, _c_int,
                          _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _c_int, _vp, _c_int, _c_dbl,
                          _vp, _vp, _vp, _c_int, _c_int, _c_dbl, _vp], _c_int),

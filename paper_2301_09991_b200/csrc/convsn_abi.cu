@@ -91,6 +91,29 @@ void launch_pg_k_x2(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>
     pg_diffusivity_x2_kernel<L, EMA, VEC><<<grid, block, sm, st>>>(a);
 }
 
+template <int L, bool EMA, int VEC>
+void launch_pg_grad_x2(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a, float* gx,
+                       float* gy, int gh) {
+    constexpr size_t sm = pg_grad_x2_smem<L, EMA>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_grad_x2_kernel<L, EMA, VEC>, sm); attr = true; }
+    pg_grad_x2_kernel<L, EMA, VEC><<<grid, block, sm, st>>>(a, gx, gy, gh);
+}
+
+template <int L, int VEC>
+void launch_pg_kcoef_x2(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a,
+                        const float* gx, const float* gy, int gh) {
+    constexpr size_t sm = pg_kcoef_x2_smem<L>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_kcoef_x2_kernel<L, VEC>, sm); attr = true; }
+    pg_kcoef_x2_kernel<L, VEC><<<grid, block, sm, st>>>(a, gx, gy, gh);
+}
+
+// workspace of the split diffusivity path: psi_x, psi_y on the +-2l band (halo 2l)
+inline int64_t grad_field_elems(const csn_geom* g, int L) {
+    return (int64_t)(g->nx + 4 * L) * (g->ny + 4 * L) * g->nd * g->ng;
+}
+
 template <class Real, int L, bool EMA, int VEC>
 void launch_pg_k(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<Real>& a) {
     constexpr size_t sm = pg_k_smem<Real, L, EMA>();
@@ -181,7 +204,7 @@ template <class Real, int L>
 int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const void* psi,
               int psi_h, const void* avg_in, int avg_in_h, void* avg_out, int avg_out_h,
               int avg_mode, double theta, const void* mu, const void* nu, void* kx, void* ky,
-              int k_h, cudaStream_t st) {
+              int k_h, void* work, cudaStream_t st) {
     constexpr int T = 2 * L + 1;
     constexpr int KT = KTile<Real, L>::value;
     constexpr int TXO = KT - 2 * L;
@@ -203,7 +226,37 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
     a.kx = (Real*)kx; a.ky = (Real*)ky; a.k_h = k_h;
     constexpr int V = 16 / sizeof(Real);
     const bool vec = vec_ok(g, V);
-    if constexpr (sizeof(Real) == 4 && L <= 3) {   // packed fp32x2, a lane per channel pair
+    if constexpr (sizeof(Real) == 4 && L <= 3) {
+      if (work) {   // split: K2a gradients -> workspace -> K2b coefficients
+        float* gxp = (float*)work;
+        float* gyp = gxp + grad_field_elems(g, L);
+        const int gh = 2 * L;
+        const int gy = (int)cdiv((int64_t)g->nd * g->ng, X2_CC);
+        dim3 block(32, PG_TX);
+        {
+            const int gx = (int)cdiv(g->nx + 4 * L, PG_TX);
+            a.ly = pick_ly((int64_t)gx * gy, g->ny + 4 * L, T);
+            dim3 grid(gx, gy, (int)cdiv(g->ny + 4 * L, a.ly));
+            if (avg_mode == 2) {
+                if (vec) launch_pg_grad_x2<L, true, V>(grid, block, st, a, gxp, gyp, gh);
+                else launch_pg_grad_x2<L, true, 1>(grid, block, st, a, gxp, gyp, gh);
+            } else {
+                if (vec) launch_pg_grad_x2<L, false, V>(grid, block, st, a, gxp, gyp, gh);
+                else launch_pg_grad_x2<L, false, 1>(grid, block, st, a, gxp, gyp, gh);
+            }
+            CSN_CHECK_LAUNCH();
+        }
+        {
+            const int gx = (int)cdiv(g->nx + 2 * L, PG_TX);
+            a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T);
+            dim3 grid(gx, gy, (int)cdiv(g->ny + 2 * L, a.ly));
+            if (vec) launch_pg_kcoef_x2<L, V>(grid, block, st, a, gxp, gyp, gh);
+            else launch_pg_kcoef_x2<L, 1>(grid, block, st, a, gxp, gyp, gh);
+            CSN_CHECK_LAUNCH();
+        }
+        return CSN_OK;
+      }
+      {   // fused two-stage, packed fp32x2, a lane per channel pair
         constexpr int TXO2 = X2_KT - 2 * L;
         const int gx = (int)cdiv(g->nx + 2 * L, TXO2);
         const int gy = (int)cdiv((int64_t)g->nd * g->ng, X2_CC);
@@ -219,6 +272,7 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
         }
         CSN_CHECK_LAUNCH();
         return CSN_OK;
+      }
     }
     const int gx = (int)cdiv(g->nx + 2 * L, TXO);
     const int gy = (int)cdiv((int64_t)g->nd * g->ng, PG_CC);
@@ -445,11 +499,17 @@ int csn_pg_diffusivities(int dtype, int order, const csn_geom* g, const double* 
                          const double* cfg, const void* psi, int psi_halo, const void* avg_in,
                          int avg_in_halo, void* avg_out, int avg_out_halo, int avg_mode,
                          double theta, const void* mu, const void* nu, void* kx, void* ky,
-                         int k_halo, void* stream) {
+                         int k_halo, void* work, void* stream) {
     if (!geom_ok(g) || !taps || !cfg || !psi || !mu || !nu || !kx || !ky) return CSN_E_ARG;
     if (dtype != CSN_F32 && dtype != CSN_F64) return CSN_E_DTYPE;
     ORDER_DISPATCH(pg_k_impl, g, taps, cfg, psi, psi_halo, avg_in, avg_in_halo, avg_out,
-                   avg_out_halo, avg_mode, theta, mu, nu, kx, ky, k_halo, S(stream));
+                   avg_out_halo, avg_mode, theta, mu, nu, kx, ky, k_halo, work, S(stream));
+}
+
+int64_t csn_pg_workspace_size(int dtype, const csn_geom* g, int order) {
+    if (!geom_ok(g)) return -CSN_E_ARG;
+    if (dtype != CSN_F32 || order < 1 || order > 3) return 0;
+    return 2 * grad_field_elems(g, order) * (int64_t)sizeof(float);
 }
 
 int csn_pg_residual(int dtype, int order, const csn_geom* g, const double* taps,

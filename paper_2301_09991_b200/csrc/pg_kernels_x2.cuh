@@ -439,4 +439,160 @@ pg_diffusivity_x2_kernel(const PGKArgs<float> a) {
     cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------------
+// K2 split through a workspace (fp32, L <= 3): the two stages of the diffusivity
+// kernel as two balanced y-marches (R/discretisation.py:114-161).  The fused
+// two-stage CTA recomputes 2l stage-1 columns per 10 outputs and idles its 2l edge
+// warps through stage 2 behind a CTA-wide barrier; through HBM each stage runs on
+// every lane with no x redundancy, at 8 B/DOF written + read for psi_x, psi_y.
+// Operation order is the fused kernel's, so k is bit-identical.
+//   K2a pg_grad_x2_kernel:  pbar = (1-theta) pbar_old + theta psi (written back on the
+//       owned interior), psi_x = M_y G_x pbar / dx, psi_y = G_y M_x pbar / dy on the
+//       +-2l band;
+//   K2b pg_kcoef_x2_kernel: R = alpha_r mu (M_y M_x psi_x - psi_x), k on the +-l band.
+// ---------------------------------------------------------------------------------
+template <int L, bool EMA>
+constexpr size_t pg_grad_x2_smem() {
+    return (size_t)PGStages<float>::value * (EMA ? 2 : 1) * (PG_TX + 2 * L) * X2_CC * sizeof(float);
+}
+
+template <int L, bool EMA, int VEC>
+__global__ void __launch_bounds__(32 * PG_TX, 3)
+pg_grad_x2_kernel(const PGKArgs<float> a, float* __restrict__ gx_out,
+                  float* __restrict__ gy_out, int gh) {
+    using TP = UnitTaps<L>;
+    constexpr int T = 2 * L + 1;
+    constexpr int CC = X2_CC;
+    constexpr int W = PG_TX + 2 * L;
+    constexpr int NT = 32 * PG_TX;
+    constexpr int G4 = CC / VEC;
+    constexpr int NI = (W * G4 + NT - 1) / NT;
+    constexpr int NF = EMA ? 2 : 1;               // psi (, pbar_old)
+    constexpr int S = PGStages<float>::value;
+    constexpr int FS = W * CC;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    float* sm = reinterpret_cast<float*>(smraw);
+
+    const Geo& g = a.g;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = ty * 32 + tx;
+    const int c0 = blockIdx.y * CC;
+    const int c = c0 + 2 * tx;
+    const bool cval = c < g.C;
+    const int cs = cval ? c : g.C - 2;
+    const int x0 = -2 * L + (int)blockIdx.x * PG_TX;         // band x in [-2l, nx+2l)
+    const int x = x0 + ty;
+    const bool act = x < g.nx + 2 * L && cval;
+    const int ya = -2 * L + (int)blockIdx.z * a.ly;          // band y in [-2l, ny+2l)
+    const int yb = min(g.ny + 2 * L, ya + a.ly);
+    const int ox0 = max(x0, 0), ox1 = min(x0 + PG_TX, g.nx);
+    const int oy0 = max(ya, 0), oy1 = min(yb, g.ny);
+    const float2 inv_dx = bc2(a.inv_dx), inv_dy = bc2(a.inv_dy);
+    const float omt = a.omt, theta = a.theta;
+    const bool write_avg = a.avg_mode != 0;
+    const int nsteps = 2 * L + (int)(((yb - ya) + T - 1) / T) * T;
+    const int64_t ob = fidx(act ? x : 0, 0, cs, g.ny, gh, g.C);
+
+    FieldDesc fd[2] = {{a.psi, a.psi_h}, {a.avg_in, a.avg_in_h}};
+    Stager<float, VEC, NI, NF, 0, CC> st;
+    st.init(g, fd, x0 - L, W, c0, 0, a.mu, a.nu, tid, NT);
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(sm);
+    constexpr unsigned FSB = FS * sizeof(float);
+    float* own_ptr[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+        const int e = tid + i * NT;
+        const int xi = e / G4, q = e % G4;
+        const int xg = x0 - L + xi, cc = c0 + q * VEC;
+        own_ptr[i] = (write_avg && e < W * G4 && cc < g.C && xg >= ox0 && xg < ox1)
+                         ? a.avg_out + fidx(xg, 0, cc, g.ny, a.avg_out_h, g.C) : nullptr;
+    }
+    const int lane = ty * CC + 2 * tx;
+    float2 rG[T], rM[T];   // x pass G, M of pbar by lead row (step mod T)
+
+#pragma unroll
+    for (int k = 0; k < S - 1; ++k) {
+        if (k < nsteps) st.issue(ya - L + k, sbase + k * NF * FSB, FSB, a.psi);
+        cp_async_commit();
+    }
+    // K: step (lead row ya - L + K); KR = K mod T (compile time); output row Y = lead - l
+#define K2A_STEP(K, KR, OUT, Y)                                                           {                                                                                         const int k_ = (K);                                                                   const int yl_ = ya - L + k_;                                                          cp_async_wait<S - 2>();                                                               float* buf_ = sm + (size_t)(k_ % S) * NF * FS;                                        if (EMA || write_avg) {                                                                   const bool own_row_ = yl_ >= oy0 && yl_ < oy1;                                       _Pragma("unroll") for (int i = 0; i < NI; ++i) {                                          const int e = tid + i * NT;                                                           if (e < W * G4) {                                                                         float* p_ = buf_ + (e / G4) * CC + (e % G4) * VEC;                                    float pv_[VEC];                                                                       _Pragma("unroll") for (int vv = 0; vv < VEC; ++vv) {                                      pv_[vv] = p_[vv];                                                                     if (EMA) pv_[vv] = p_[FS + vv] * omt + theta * pv_[vv];                               p_[vv] = pv_[vv];                                                                 }                                                                                     if (own_ptr[i] && own_row_) {                                                             float* o_ = own_ptr[i] + (int64_t)yl_ * g.C;                                          _Pragma("unroll") for (int vv = 0; vv < VEC; ++vv) o_[vv] = pv_[vv];                     }                                                                                 }                                                                                 }                                                                                 }                                                                                     __syncthreads();                                                                      {                                                                                         float2 ag_ = bc2(0.f), am_ = ag_;                                                     const float* bp_ = buf_ + lane;                                                       _Pragma("unroll") for (int t = 0; t < T; ++t) {                                           const float2 p_ = ld2(bp_ + t * CC);                                                  ag_ = fma2c((float)TP::g(t), p_, ag_);                                                am_ = fma2c((float)TP::m(t), p_, am_);                                            }                                                                                     rG[(KR)] = ag_;                                                                       rM[(KR)] = am_;                                                                   }                                                                                     if ((OUT) && act && (Y) < yb) {                                                           float2 px_ = bc2(0.f), py_ = px_;                                                     _Pragma("unroll") for (int b = 0; b < T; ++b) {                                           px_ = fma2c((float)TP::m(b), rG[((KR) + 1 + b) % T], px_);                            py_ = fma2c((float)TP::g(b), rM[((KR) + 1 + b) % T], py_);                        }                                                                                     const int64_t o_ = ob + (int64_t)(Y) * g.C;                                           st2(gx_out + o_, mul2(px_, inv_dx));                                                  st2(gy_out + o_, mul2(py_, inv_dy));                                              }                                                                                     if (k_ + S - 1 < nsteps)                                                                  st.issue(ya - L + k_ + S - 1, sbase + ((k_ + S - 1) % S) * NF * FSB, FSB, a.psi);         cp_async_commit();                                                                }
+#pragma unroll
+    for (int k = 0; k < 2 * L; ++k) K2A_STEP(k, k % T, false, 0);
+    int kb = 2 * L;
+    for (int y0 = ya; y0 < yb; y0 += T, kb += T) {
+#pragma unroll
+        for (int s = 0; s < T; ++s) K2A_STEP(kb + s, (2 * L + s) % T, true, y0 + s);
+    }
+#undef K2A_STEP
+    cp_async_wait<0>();
+}
+
+template <int L>
+constexpr size_t pg_kcoef_x2_smem() {
+    return (size_t)X2Stages<L>::value * 2 * (PG_TX + 2 * L) * X2_CC * sizeof(float);
+}
+
+template <int L, int VEC>
+__global__ void __launch_bounds__(32 * PG_TX, 3)
+pg_kcoef_x2_kernel(const PGKArgs<float> a, const float* __restrict__ gx_in,
+                   const float* __restrict__ gy_in, int gh) {
+    using TP = UnitTaps<L>;
+    constexpr int T = 2 * L + 1;
+    constexpr int CC = X2_CC;
+    constexpr int W = PG_TX + 2 * L;
+    constexpr int NT = 32 * PG_TX;
+    constexpr int G4 = CC / VEC;
+    constexpr int NI = (W * G4 + NT - 1) / NT;
+    constexpr int NF = 2;                          // psi_x, psi_y
+    constexpr int S = X2Stages<L>::value;
+    constexpr int P = S - L - 1;
+    constexpr int FS = W * CC;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    float* sm = reinterpret_cast<float*>(smraw);
+
+    const Geo& g = a.g;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = ty * 32 + tx;
+    const int c0 = blockIdx.y * CC;
+    const int c = c0 + 2 * tx;
+    const bool cval = c < g.C;
+    const int cs = cval ? c : g.C - 2;
+    const int n0 = cs / g.ng, n1 = (cs + 1) / g.ng;
+    const float mu0 = a.mu[n0], mu1 = a.mu[n1], nu0 = a.nu[n0], nu1 = a.nu[n1];
+    const int x0 = -L + (int)blockIdx.x * PG_TX;             // band x in [-l, nx+l)
+    const int x = x0 + ty;
+    const bool act = x < g.nx + L && cval;
+    const int ya = -L + (int)blockIdx.z * a.ly;              // band y in [-l, ny+l)
+    const int yb = min(g.ny + L, ya + a.ly);
+    const int nsteps = 2 * L + (int)(((yb - ya) + T - 1) / T) * T;
+    const int64_t kb0 = fidx(act ? x : 0, 0, cs, g.ny, a.k_h, g.C);
+
+    FieldDesc fd[2] = {{gx_in, gh}, {gy_in, gh}};
+    Stager<float, VEC, NI, NF, 0x3, CC> st;        // both band fields, zero outside +-2l
+    st.init(g, fd, x0 - L, W, c0, 2 * L, a.mu, a.nu, tid, NT);
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(sm);
+    constexpr unsigned FSB = FS * sizeof(float);
+    constexpr unsigned SLOTB = NF * FSB;
+    const int lane = ty * CC + 2 * tx;
+    float2 r2x[T], r2y[T];   // M_x psi_x, M_x psi_y by lead row (step mod T)
+
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        if (k < nsteps) st.issue(ya - L + k, sbase + k * SLOTB, FSB, gx_in);
+        cp_async_commit();
+    }
+    int slot = 0;
+#define K2B_STEP(K, KR, OUT, Y)                                                           {                                                                                         const int k_ = (K);                                                                   cp_async_wait<P - 1>();                                                               __syncthreads();                                                                      const float* buf_ = sm + slot * (NF * FS) + lane;                                     float2 mx_ = bc2(0.f), my_ = mx_;                                                     _Pragma("unroll") for (int t = 0; t < T; ++t) {                                           mx_ = fma2c((float)TP::m(t), ld2(buf_ + t * CC), mx_);                                my_ = fma2c((float)TP::m(t), ld2(buf_ + FS + t * CC), my_);                       }                                                                                     r2x[(KR)] = mx_;                                                                      r2y[(KR)] = my_;                                                                      if ((OUT) && act && (Y) < yb) {                                                           float2 mmx = bc2(0.f), mmy = mmx;                                                     _Pragma("unroll") for (int b = 0; b < T; ++b) {                                           mmx = fma2c((float)TP::m(b), r2x[((KR) + 1 + b) % T], mmx);                           mmy = fma2c((float)TP::m(b), r2y[((KR) + 1 + b) % T], mmy);                       }                                                                                     const int cs_ = slot >= L ? slot - L : slot - L + S;                                  const float* cb = sm + cs_ * (NF * FS) + L * CC + lane;                               const float2 pxc = ld2(cb), pyc = ld2(cb + FS);                                       const float2 rx = mul2(make_float2(a.alpha_r * mu0, a.alpha_r * mu1), sub2(mmx, pxc));             const float2 ry = mul2(make_float2(a.alpha_r * nu0, a.alpha_r * nu1), sub2(mmy, pyc));             const float amu[2] = {fabsf(mu0), fabsf(mu1)}, anu[2] = {fabsf(nu0), fabsf(nu1)};             const float pxv[2] = {pxc.x, pxc.y}, pyv[2] = {pyc.x, pyc.y};                         const float rxv[2] = {rx.x, rx.y}, ryv[2] = {ry.x, ry.y};                             float kx[2], ky[2];                                                                   _Pragma("unroll") for (int h = 0; h < 2; ++h) {                                           const float bx = fast_div(a.a_abs * a.dx * fabsf(rxv[h]), a.eps + fabsf(pxv[h]));                 const float sx = fast_div(a.a_sq * a.dx * (rxv[h] * rxv[h]),                                                    a.eps + amu[h] * (pxv[h] * pxv[h]));                        const float by = fast_div(a.a_abs * a.dy * fabsf(ryv[h]), a.eps + fabsf(pyv[h]));                 const float sy = fast_div(a.a_sq * a.dy * (ryv[h] * ryv[h]),                                                    a.eps + anu[h] * (pyv[h] * pyv[h]));                        /* NaN candidate -> 0 (numpy minimum + nan_to_num); dx|mu| is finite */                 kx[h] = (bx != bx || sx != sx) ? 0.f : fminf(a.dx * amu[h], fminf(bx, sx));                 ky[h] = (by != by || sy != sy) ? 0.f : fminf(a.dy * anu[h], fminf(by, sy));             }                                                                                     const int64_t o = kb0 + (int64_t)(Y) * g.C;                                           st2(a.kx + o, make_float2(kx[0], kx[1]));                                             st2(a.ky + o, make_float2(ky[0], ky[1]));                                         }                                                                                     if (k_ + P < nsteps) {                                                                    const int is_ = slot + P >= S ? slot + P - S : slot + P;                              st.issue(ya - L + k_ + P, sbase + is_ * SLOTB, FSB, gx_in);                       }                                                                                     cp_async_commit();                                                                    slot = slot + 1 == S ? 0 : slot + 1;                                              }
+#pragma unroll
+    for (int k = 0; k < 2 * L; ++k) K2B_STEP(k, k % T, false, 0);
+    int kb = 2 * L;
+    for (int y0 = ya; y0 < yb; y0 += T, kb += T) {
+#pragma unroll
+        for (int s = 0; s < T; ++s) K2B_STEP(kb + s, (2 * L + s) % T, true, y0 + s);
+    }
+#undef K2B_STEP
+    cp_async_wait<0>();
+}
+
 }  // namespace csn

@@ -102,9 +102,20 @@ def _check_order(fs, halo):
         raise ValueError(f"PG diffusivities need halo >= {3 * l}, field has {halo}")
 
 
+def diffusivities_workspace(psi_data, gm, order):
+    """Workspace tensor for the split fp32 diffusivity path (None where it has none)."""
+    nbytes = _lib.load().csn_pg_workspace_size(_lib.dtype_code(psi_data), gm, order)
+    if nbytes < 0:
+        _lib.check(int(nbytes), "csn_pg_workspace_size")
+    if nbytes == 0:
+        return None
+    return torch.empty(int(nbytes) // 4, dtype=torch.float32, device=psi_data.device)
+
+
 def diffusivities_into(psi_data, grid, n_dir, n_group, n_a, fs, cfg, mu, nu, kx, ky, k_halo,
-                       avg_in=None, avg_out=None, avg_mode=0, theta=1.0, psi_halo=None, gm=None):
-    """Launch the fused averaging + k kernel (K2)."""
+                       avg_in=None, avg_out=None, avg_mode=0, theta=1.0, psi_halo=None, gm=None,
+                       work=None):
+    """Launch the averaging + k kernels (K2; K2a + K2b through ``work`` when given)."""
     taps_arr = fs.taps()
     cfg_arr = cfg.host_cfg(fs.order)
     taps_p = taps_arr.ctypes.data_as(_lib._DP)
@@ -115,7 +126,7 @@ def diffusivities_into(psi_data, grid, n_dir, n_group, n_a, fs, cfg, mu, nu, kx,
     _lib.call("csn_pg_diffusivities", _lib.dtype_code(psi_data), fs.order, gm, taps_p, cfg_p,
               _lib.ptr(psi_data), h, _lib.ptr(avg_in), h, _lib.ptr(avg_out), h, avg_mode,
               float(theta), _lib.ptr(mu), _lib.ptr(nu), _lib.ptr(kx), _lib.ptr(ky), k_halo,
-              _lib.stream())
+              _lib.ptr(work), _lib.stream())
 
 
 def pg_anisotropic_diffusivities(psi, fs, quad, cfg, grads=None):

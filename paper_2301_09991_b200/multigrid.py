@@ -16,7 +16,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .discretisation import (PGConfig, diffusivities_into, jacobi_diagonal, pg_residual_launch,
+from .discretisation import (PGConfig, diffusivities_into, diffusivities_workspace,
+                             jacobi_diagonal, pg_residual_launch,
                              sigma_tensor, source_tensor)
 from .filters import build_upwind_filters
 from .grid import Field, GridSpec, apply_boundary, default_device
@@ -381,6 +382,7 @@ class CycleEngine:
         self.res_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
         self.psi_alt = None
         self.k_scratch = None
+        self.k_work = None         # (key, workspace of the split diffusivity kernels)
         self.probe = None          # {kernel name: [(start event, end event)]} when timing
         self.use_graphs = True     # replay recurring cycle plans from captured CUDA graphs
         self._graphs = {}
@@ -574,9 +576,12 @@ class CycleEngine:
                 if avg_in is not None:
                     self._hook_exchange("avg", avg_in, reach)
                 t = self._t0()
+                if self.k_work is None or self.k_work[0] != (fs.order, psi_in.dtype):
+                    self.k_work = ((fs.order, psi_in.dtype),
+                                   diffusivities_workspace(psi_in, self.geoms[0], fs.order))
                 diffusivities_into(psi_in, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky,
                                    g.halo, avg_in=avg_in, avg_out=avg_out, avg_mode=mode,
-                                   theta=theta, gm=self.geoms[0])
+                                   theta=theta, gm=self.geoms[0], work=self.k_work[1])
                 self._t1("pg_diffusivity", t)
             ema = plan["ema"]
             t = self._t0()
