@@ -374,13 +374,15 @@ int csn_apply_boundary(int dtype, const csn_geom* g, void* f, int halo, const vo
     if (!geom_ok(g) || !f || !mu || !nu || halo < 0) return CSN_E_ARG;
     if (halo == 0) return CSN_OK;
     Geo d = make_geo(*g);
-    const int64_t total = ((int64_t)2 * halo * (g->ny + 2 * halo) + (int64_t)g->nx * 2 * halo) * d.C;
+    const int64_t cells = (int64_t)2 * halo * (g->ny + 2 * halo) + (int64_t)g->nx * 2 * halo;
+    if (cells > INT32_MAX) return CSN_E_ARG;
+    dim3 grid((unsigned)cdiv(d.C, 256), (unsigned)(cells < 65535 ? cells : 65535));
     if (dtype == CSN_F32)
-        boundary_kernel<float><<<grid1d(total), 256, 0, S(stream)>>>(d, (float*)f, halo,
-                                                                      (const float*)mu, (const float*)nu);
+        boundary_kernel<float><<<grid, 256, 0, S(stream)>>>(d, (float*)f, halo, (const float*)mu,
+                                                            (const float*)nu);
     else if (dtype == CSN_F64)
-        boundary_kernel<double><<<grid1d(total), 256, 0, S(stream)>>>(d, (double*)f, halo,
-                                                                       (const double*)mu, (const double*)nu);
+        boundary_kernel<double><<<grid, 256, 0, S(stream)>>>(d, (double*)f, halo,
+                                                             (const double*)mu, (const double*)nu);
     else return CSN_E_DTYPE;
     CSN_CHECK_LAUNCH();
     return CSN_OK;

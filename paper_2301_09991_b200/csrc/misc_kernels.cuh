@@ -96,30 +96,29 @@ __global__ void __launch_bounds__(256) prolong_kernel(const ProlongArgs<Real> a)
 template <class Real>
 __global__ void __launch_bounds__(256)
 boundary_kernel(Geo g, Real* f, int h, const Real* mu, const Real* nu) {
-    // iterate over halo cells only: rows [0, h) and [nx+h, nx+2h) fully, plus the
-    // left/right h columns of the interior rows
+    // halo cells only: storage rows [0, h) and [nx+h, nx+2h) fully, plus the h
+    // columns on either side of the interior rows.  blockIdx.y walks the halo cells
+    // (32-bit index math, done once per cell), threads walk the contiguous channels.
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= g.C) return;
     const int NY = g.ny + 2 * h;
-    const int64_t n_rowcells = (int64_t)2 * h * NY;
-    const int64_t n_colcells = (int64_t)g.nx * 2 * h;
-    const int64_t total = (n_rowcells + n_colcells) * g.C;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(e % g.C);
-        int64_t k = e / g.C;
+    const int n_rowcells = 2 * h * NY;
+    const int n_cells = n_rowcells + g.nx * 2 * h;
+    const int n = c / g.ng;
+    const bool mpos = mu[n] > Real(0), npos = nu[n] > Real(0);
+    for (int k = blockIdx.y; k < n_cells; k += gridDim.y) {
         int xs, ys;   // storage coordinates
         if (k < n_rowcells) {
-            const int r = (int)(k / NY);
-            ys = (int)(k % NY);
+            const int r = k / NY;
+            ys = k - r * NY;
             xs = r < h ? r : g.nx + r;
         } else {
-            k -= n_rowcells;
-            const int r = (int)(k / (2 * h));
-            const int cidx = (int)(k % (2 * h));
+            const int kk = k - n_rowcells;
+            const int r = kk / (2 * h);
+            const int cidx = kk - r * 2 * h;
             xs = h + r;
             ys = cidx < h ? cidx : g.ny + cidx;
         }
-        const int n = c / g.ng;
-        const bool mpos = mu[n] > Real(0), npos = nu[n] > Real(0);
         int x = xs - h, y = ys - h;
         Real v = Real(0);
         if (resolve_vac(x, y, g, mpos, npos)) v = f[fidx(x, y, c, g.ny, h, g.C)];

@@ -120,12 +120,23 @@ pg_residual_x2_kernel(const PGResidArgs<float> a) {
     }
     double l1 = 0.0;
     int slot = 0;   // staging slot of the current step (k mod S)
+    // sigma, q of the next output row, loaded a step ahead of use
+    float2 sgN = bc2(0.f), qN = bc2(0.f);
+    if (act) {
+        sgN = make_float2(sig0[ya * g.ng], sig1[ya * g.ng]);
+        qN = make_float2(q0[ya * qst], q1[ya * qst]);
+    }
 
     // One step: stage-ready lead row j = ya - L + K; SK = slot of output row j - L in
     // the pending rings; OUT: output row j - L = Y is complete after this step.
 #define X2_STEP(K, SK, OUT, Y)                                                        \
     {                                                                                 \
         const int k_ = (K);                                                           \
+        float2 sg_ = sgN, q_ = qN;                                                    \
+        if ((OUT) && act && (Y) + 1 < yb) {                                           \
+            sgN = make_float2(sig0[((Y) + 1) * g.ng], sig1[((Y) + 1) * g.ng]);       \
+            qN = make_float2(q0[((Y) + 1) * qst], q1[((Y) + 1) * qst]);              \
+        }                                                                             \
         cp_async_wait<P - 1>();                                                       \
         float* buf_ = sm + slot * (NF * FS);                                          \
         if (SWEEP) {                                                                  \
@@ -194,8 +205,6 @@ pg_residual_x2_kernel(const PGResidArgs<float> a) {
             const int cs_ = slot >= L ? slot - L : slot - L + S;                      \
             const float* cb_ = sm + cs_ * (NF * FS) + L * CC + lane_off;              \
             const float2 pc_ = ld2(cb_), kxc_ = ld2(cb_ + FS), kyc_ = ld2(cb_ + 2 * FS); \
-            const float2 sg_ = make_float2(sig0[y_ * g.ng], sig1[y_ * g.ng]);        \
-            const float2 q_ = make_float2(q0[y_ * qst], q1[y_ * qst]);               \
             float2 r_ = fma2(hx, mul2(kxc_, rB[SK]), rA[SK]);                         \
             r_ = fma2(hy, mul2(kyc_, rC[SK]), r_);                                    \
             r_ = sub2(fma2(pc_, add2(rD[SK], sg_), r_), q_);                          \
