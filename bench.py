@@ -119,12 +119,12 @@ def workload(name, nx=None):
     raise SystemExit(f"unknown config {name}")
 
 
-def options_for(P, pd, dtype, cycles=None):
+def options_for(P, pd, dtype, cycles=None, fold=False):
     o = dict(pd.options)
     pg = o.pop("pg", None)
     if cycles is not None:
         o["mg_iters"] = cycles
-    return P.SolverOptions(**o, pg=P.PGConfig(**(pg or {})), dtype=dtype)
+    return P.SolverOptions(**o, pg=P.PGConfig(**(pg or {})), dtype=dtype, fold_z=fold)
 
 
 def per_dof_bytes(kernel, esz):
@@ -134,8 +134,8 @@ def per_dof_bytes(kernel, esz):
 
 def bytes_model(pd, hier, live):
     """Algorithmic fp32 bytes per cycle."""
-    n0 = pd.dof()
-    coarse = sum(l.grid.nx * l.grid.ny * l.quad.n_dir * pd.n_groups for l in hier.levels[1:])
+    lv = [l.grid.nx * l.grid.ny * l.quad.n_dir * pd.n_groups for l in hier.levels]
+    n0, coarse = lv[0], sum(lv[1:])
     if pd.options["scheme"] == "upwind" or pd.options.get("pg", {}).get("alpha_r", 3.0) == 0.0:
         return 28 * n0 + 16 * coarse
     # live: K2 20 + K3 16 + finest correction 8 + K5 20; frozen: the EMA (12 B standalone)
@@ -222,7 +222,7 @@ def run_b200(args, rank, world, local_rank):
     total = args.warmup + args.steps
     eigen = pd.driver == "power_iteration"
     inner = pd.inner_iters or 1
-    opts = options_for(P, pd, args.dtype, None if eigen else total)
+    opts = options_for(P, pd, args.dtype, None if eigen else total, args.fold)
     if eigen:
         opts.outer_iters = -(-total // inner)
     prob = problem_from_data(pd)
@@ -277,7 +277,7 @@ def run_b200(args, rank, world, local_rank):
                          "region (the timed region replays CUDA graphs)")
     probe = {k: [a.elapsed_time(b) for a, b in v] for k, v in (eng.probe or {}).items()}
     eng.probe = None
-    dof = pd.dof()
+    dof = pd.dof() // 2 if args.fold else pd.dof()   # DOF actually updated
     value = dof * args.steps / (ms * 1e-3)          # global DOF: strong scaling over ranks
 
     # ---- roofline of the dominant kernel (fused PG sweep, K5): 20 B/DOF fp32
@@ -354,6 +354,7 @@ def run_b200(args, rank, world, local_rank):
             "config": {"workload": f"{args.config}: " + WORKLOADS.get(args.config, ""),
                        "dof_per_cycle": dof, "nx": pd.nx, "ny": pd.ny,
                        "ordinates": 8 * pd.n_a ** 2, "groups": pd.n_groups,
+                       "fold_z": bool(args.fold),
                        "order": pd.options["order"], "scheme": pd.options["scheme"],
                        "levels": solver.setup.hierarchy.n_levels, "live_cycles": live,
                        "frozen_cycles": args.steps - live, "cuda_graphs": graphs,
@@ -407,6 +408,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--fold", action="store_true",
+                    help="z-mirror fold (half the ordinates, same flux); value counts the "
+                         "DOF actually updated, not the full-sphere equivalent")
     ap.add_argument("--graphs", default="auto", choices=["auto", "on", "off"])
     args = ap.parse_args()
     if args.warmup < 0 or args.steps < 1:

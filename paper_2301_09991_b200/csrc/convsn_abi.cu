@@ -60,11 +60,12 @@ void set_smem(K kernel, size_t bytes) {
 }
 
 // 16-byte staging needs every aligned VEC-channel group inside one octahedron face
-// (same upwind signs) and VEC | C (alignment): a face holds n_a^2 * ng channels.
+// (same upwind signs) and VEC | C (alignment): a face holds n_a^2 * ng channels
+// (8 faces, or 4 for the z-folded hemisphere).
 inline bool vec_ok(const csn_geom* g, int vec) {
     const int64_t C = (int64_t)g->nd * g->ng;
     const int64_t face = (int64_t)g->na * g->na * g->ng;
-    return C % vec == 0 && face % vec == 0 && 8 * face == C;
+    return C % vec == 0 && face % vec == 0 && C % face == 0;
 }
 
 template <class Real, int L, int MODE, int VEC>

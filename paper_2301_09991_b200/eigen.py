@@ -19,7 +19,7 @@ from .discretisation import PGConfig
 from .filters import build_convfem_filters
 from .grid import Field, GridSpec, apply_boundary, default_device, scalar_flux_into
 from .multigrid import PGState, build_hierarchy, max_levels
-from .quadrature import build_quadrature
+from .quadrature import build_quadrature, fold_z
 
 _DTYPES = {"float32": torch.float32, "float64": torch.float64,
            torch.float32: torch.float32, torch.float64: torch.float64}
@@ -42,6 +42,7 @@ class SolverOptions:
     k_avg_theta: float = 0.2
     pg: PGConfig = field(default_factory=PGConfig)
     dtype: str = "float32"          # field precision on the device ("float32" | "float64")
+    fold_z: bool = False            # carry the upper hemisphere only (exact for x-y problems)
 
     def bootstrap(self):
         if self.bootstrap_cycles is not None:
@@ -100,6 +101,8 @@ def setup_transport(problem, options):
         raise ValueError(f"unknown scheme {options.scheme!r}")
     grid = GridSpec(problem.nx, problem.ny, problem.dx, problem.dy, options.filter_halo())
     quad = build_quadrature(options.n_a)
+    if options.fold_z:
+        quad = fold_z(quad)
     fs = build_convfem_filters(options.order, problem.dx, problem.dy) \
         if options.scheme == "pg" else None
     mat = problem.material_field()
@@ -107,10 +110,6 @@ def setup_transport(problem, options):
     hier = build_hierarchy(grid, quad, mat.sigma_t, n_levels)
     return TransportSetup(grid=grid, quad=quad, filters=fs, mat=mat, hierarchy=hier,
                           options=options)
-
-
-def _geom(grid, ng, n_a):
-    return _lib.geom(grid.nx, grid.ny, 8 * n_a * n_a, ng, n_a, grid.dx, grid.dy)
 
 
 def assemble_group_source(phi, mat, lam=0.0, dtype=torch.float64, out=None, fission=None):

@@ -21,7 +21,7 @@ from .discretisation import (PGConfig, diffusivities_into, diffusivities_workspa
                              sigma_tensor, source_tensor)
 from .filters import build_upwind_filters
 from .grid import Field, GridSpec, apply_boundary, default_device
-from .quadrature import N_FACES, coarsen_quadrature
+from .quadrature import coarsen_quadrature
 
 UP_MAX_SWEEPS = 3   # sweeps per temporally blocked smoother launch (csrc/upwind_kernels.cuh)
 
@@ -478,6 +478,8 @@ class CycleEngine:
             return None
         torch.cuda.current_stream().synchronize()
         res = float(self.res_host[0])
+        if self.h.levels[0].quad.folded:    # the mirrored faces carry the same |r|
+            res *= 2.0
         if scheme == "pg" and pg_state is not None:
             pg_state.observe(res, cfg.k_freeze_rel)
         return res

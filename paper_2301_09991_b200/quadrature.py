@@ -27,6 +27,7 @@ class AngularQuadrature:
     directions: np.ndarray   # (n_dir, 3): mu, nu, xi
     weights: np.ndarray      # (n_dir,), sum 4 pi
     face_index: np.ndarray   # (n_dir,)
+    n_faces_: int = N_FACES  # 8, or 4 for the z-folded upper hemisphere (fold_z)
 
     def __post_init__(self):
         for arr in (self.directions, self.weights, self.face_index):
@@ -34,7 +35,11 @@ class AngularQuadrature:
 
     @property
     def n_faces(self):
-        return N_FACES
+        return self.n_faces_
+
+    @property
+    def folded(self):
+        return self.n_faces_ != N_FACES
 
     @property
     def n_dir(self):
@@ -138,12 +143,31 @@ def coarsen_quadrature(quad):
     if quad.n_a < 2:
         raise ValueError("cannot coarsen: already at one patch per face")
     m = quad.n_a // 2
-    w = quad.weights.reshape(N_FACES, m, 2, m, 2)
-    d = quad.directions.reshape(N_FACES, m, 2, m, 2, 3)
+    nf = quad.n_faces
+    w = quad.weights.reshape(nf, m, 2, m, 2)
+    d = quad.directions.reshape(nf, m, 2, m, 2, 3)
     wc = w.sum(axis=(2, 4))
     dc = (d * w[..., None]).sum(axis=(2, 4)) / wc[..., None]
     return AngularQuadrature(n_a=m, directions=dc.reshape(-1, 3), weights=wc.reshape(-1),
-                             face_index=np.repeat(np.arange(N_FACES), m * m))
+                             face_index=np.repeat(np.arange(nf), m * m), n_faces_=nf)
+
+
+def fold_z(quad):
+    """Exact z-mirror fold of a 2D problem: faces 4-7 are the
+    xi -> -xi mirrors of faces 0-3 with identical (mu, nu, w) (R/quadrature.py:28-31),
+    and nothing in an x-y problem depends on xi, so psi stays mirror-symmetric through
+    every operator.  Carrying faces 0-3 with doubled weights gives the same scalar
+    flux with half the DOF.  Face-major storage keeps 2x2 coarsening a reshape."""
+    if quad.folded:
+        raise ValueError("quadrature is already folded")
+    half = quad.n_dir // 2
+    lo, hi = quad.directions[:half], quad.directions[half:]
+    if not (np.array_equal(lo[:, :2], hi[:, :2]) and np.array_equal(lo[:, 2], -hi[:, 2])
+            and np.array_equal(quad.weights[:half], quad.weights[half:])):
+        raise ValueError("quadrature is not z-mirror symmetric")
+    return AngularQuadrature(n_a=quad.n_a, directions=lo.copy(),
+                             weights=2.0 * quad.weights[:half],
+                             face_index=quad.face_index[:half].copy(), n_faces_=N_FACES // 2)
 
 
 def quadrature_to_csv(quad, stream):

@@ -312,3 +312,31 @@ def test_reference_benchmarks_with_bootstrap(P, dtype, tol):
                                atol=tol * float(g["boot"][0]))
     h = g["residual_history"]
     np.testing.assert_allclose(res.residual_history, h, rtol=tol * 10, atol=tol * float(h[0]))
+
+
+@pytest.mark.parametrize("tag,dtype,tol", [("c2_reduced", "float64", 1e-11),
+                                           ("c3_reduced", "float64", 1e-11),
+                                           ("c2_reduced", "float32", 2e-6)])
+def test_z_fold_matches_full_sphere(P, tag, dtype, tol):
+    """SolverOptions(fold_z=True) carries faces 0-3 with doubled weights:
+    same flux, k, residual history and PGState decisions as the full 8-face solve."""
+    from paper_2301_09991_b200 import benchmarks as B
+    from paper_2301_09991_b200.problems import problem_from_data
+    pd = DRIVERS[tag][0](B)
+    runs = []
+    for fold in (False, True):
+        o = dict(pd.options)
+        pg = o.pop("pg", None)
+        opts = P.SolverOptions(**o, pg=P.PGConfig(**(pg or {})), dtype=dtype, fold_z=fold)
+        prob = problem_from_data(pd)
+        if pd.driver == "fixed_source":
+            runs.append(P.solve_fixed_source(prob, opts))
+        else:
+            runs.append(P.power_iteration(prob, opts, inner_iters=pd.inner_iters))
+    full, half = runs
+    assert half.psi.data.shape[2] * 2 == full.psi.data.shape[2]
+    assert rel_l2(half.phi, full.phi) < tol
+    assert _log(half).tolist() == _log(full).tolist()
+    np.testing.assert_allclose(half.residual_history, full.residual_history, rtol=tol * 10)
+    if pd.driver != "fixed_source":
+        np.testing.assert_allclose(half.history, full.history, rtol=tol)

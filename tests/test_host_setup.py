@@ -177,3 +177,18 @@ def test_product_path_fails_loudly_without_cuda():
     import paper_2301_09991_b200 as P
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         P.Field(P.GridSpec(4, 4, 1.0, 1.0, 1), 8, 1)
+
+
+def test_z_fold_quadrature():
+    from paper_2301_09991_b200.quadrature import build_quadrature, coarsen_quadrature, fold_z
+    q = build_quadrature(8)
+    f = fold_z(q)
+    assert f.n_dir == q.n_dir // 2 and f.n_faces == 4 and f.folded
+    assert abs(f.weights.sum() - 4 * np.pi) < 1e-12
+    assert np.all(f.directions[:, 2] > 0)
+    # coarsening commutes with the fold (weights exactly 2x, same directions)
+    cf, cq = coarsen_quadrature(f), coarsen_quadrature(q)
+    np.testing.assert_array_equal(cf.weights, 2.0 * cq.weights[:cf.n_dir])
+    np.testing.assert_array_equal(cf.directions, cq.directions[:cf.n_dir])
+    with pytest.raises(ValueError):
+        fold_z(f)
