@@ -352,6 +352,78 @@ class Solver:
             self.step()
         return self.result()
 
+    # ------------------------------------------------------------------ checkpoint
+    # Not in the reference: a solve can stop between any two
+    # cycles and resume bit-identically — psi, the PGState (decision scalars, log,
+    # averaged iterate, diffusivities), the power iteration's phi and k, the phase
+    # counters and the histories.  The frozen fission / group source of the current
+    # block are recomputed from phi_outer and k, which do not change within a block.
+    _CKPT_VERSION = 1
+
+    def _signature(self):
+        g, o = self.setup.grid, self.options
+        return {"nx": g.nx, "ny": g.ny, "halo": g.halo, "n_dir": self.setup.quad.n_dir,
+                "n_group": self.setup.mat.n_groups, "n_a": o.n_a, "order": o.order,
+                "scheme": o.scheme, "dtype": o.dtype, "fold_z": bool(o.fold_z),
+                "eigen": self.eigen}
+
+    def state_dict(self):
+        return {"version": self._CKPT_VERSION, "signature": self._signature(),
+                "phase": self.phase, "in_phase": self.in_phase, "stopped": self.stopped,
+                "outer_done": self.outer_done, "k": self.k, "k_history": list(self.k_history),
+                "history": list(self.history), "boot_history": list(self.boot_history),
+                "psi": self.psi.data.cpu().numpy(),
+                "phi_outer": self.phi_outer.cpu().numpy() if self.eigen else None,
+                "pgs": self.pgs.state_dict()}
+
+    def load_state_dict(self, d):
+        if d.get("version") != self._CKPT_VERSION:
+            raise ValueError(f"unsupported checkpoint version {d.get('version')!r}")
+        if d["signature"] != self._signature():
+            raise ValueError(f"checkpoint is for {d['signature']}, solver is {self._signature()}")
+        self.phase, self.in_phase = int(d["phase"]), int(d["in_phase"])
+        self.stopped, self.outer_done = bool(d["stopped"]), int(d["outer_done"])
+        self.k = float(d["k"])
+        self.k_history = [float(v) for v in d["k_history"]]
+        self.history = [float(v) for v in d["history"]]
+        self.boot_history = [float(v) for v in d["boot_history"]]
+        self.psi.data.copy_(torch.as_tensor(d["psi"]).reshape(self.psi.data.shape))
+        if self.eigen:
+            self.phi_outer.copy_(torch.as_tensor(d["phi_outer"]).reshape(self.phi_outer.shape))
+            if self.in_phase > 0:        # the block's frozen fission source
+                kind = self.phases[self.phase][0]
+                self._fis = self._frozen_fission(1.0 if kind == "boot" else 1.0 / self.k)
+        self._q_ready = False
+        self.pgs.load_state_dict(d["pgs"], self.psi.data, self.setup.grid, self.setup.quad)
+
+    def save_checkpoint(self, path):
+        """Write ``state_dict`` as .npz (arrays + JSON metadata, no pickles)."""
+        import json
+        d = self.state_dict()
+        arrays = {"psi": d.pop("psi")}
+        if d["phi_outer"] is not None:
+            arrays["phi_outer"] = d["phi_outer"]
+        d.pop("phi_outer")
+        pg = d.pop("pgs")
+        for k in ("avg", "kx", "ky"):
+            a = pg.pop(k)
+            if a is not None:
+                arrays["pgs_" + k] = a
+        d["pgs"] = pg
+        with open(path, "wb") as fh:
+            np.savez(fh, meta=np.array(json.dumps(d)), **arrays)
+
+    def load_checkpoint(self, path):
+        import json
+        with np.load(path, allow_pickle=False) as z:
+            d = json.loads(str(z["meta"]))
+            d["psi"] = z["psi"]
+            d["phi_outer"] = z["phi_outer"] if "phi_outer" in z.files else None
+            for k in ("avg", "kx", "ky"):
+                d["pgs"][k] = z["pgs_" + k] if "pgs_" + k in z.files else None
+        self.load_state_dict(d)
+        return self
+
     def result(self):
         setup, ng = self.setup, self.setup.mat.n_groups
         if self.eigen:

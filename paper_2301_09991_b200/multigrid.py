@@ -307,8 +307,9 @@ class PGState:
             self._avg = torch.empty_like(d)
             self._avg_grid = psi.grid
         self._avg_quad = quad if quad is not None else self._avg_quad
-        gm = _lib.geom(psi.grid.nx, psi.grid.ny, psi.n_dir, psi.n_group,
-                       int(round((psi.n_dir / 8) ** 0.5)), psi.grid.dx, psi.grid.dy)
+        na = self._avg_quad.n_a if self._avg_quad is not None else int(round((psi.n_dir / 8) ** 0.5))
+        gm = _lib.geom(psi.grid.nx, psi.grid.ny, psi.n_dir, psi.n_group, na,
+                       psi.grid.dx, psi.grid.dy)
         _lib.call("csn_ema", _lib.dtype_code(d), gm, _lib.ptr(self._avg), psi.grid.halo,
                   _lib.ptr(d), psi.grid.halo, float(self.avg_theta), 1 if first else 2,
                   _lib.stream())
@@ -348,6 +349,31 @@ class PGState:
         self.freeze_residual = resid
         self.cycles_since_best = 0
         self.log.append((self._calls, "freeze"))
+
+    _SCALARS = ("initial_residual", "frozen", "best_residual", "cycles_since_best",
+                "freeze_residual", "failed_freezes", "avg_theta", "_calls")
+
+    def state_dict(self):
+        """Host snapshot: decision scalars, log, averaged iterate and diffusivities."""
+        host = lambda t: None if t is None else t.cpu().numpy()
+        d = {k: getattr(self, k) for k in self._SCALARS}
+        d["log"] = [list(e) for e in self.log]
+        d["avg"] = host(self._avg)
+        kx, ky = self.diffusivities if self.diffusivities is not None else (None, None)
+        d["kx"], d["ky"] = host(kx), host(ky)
+        return d
+
+    def load_state_dict(self, d, like, grid, quad):
+        """Restore a ``state_dict``; ``like`` is a device tensor of the field shape."""
+        for k in self._SCALARS:
+            setattr(self, k, d[k])
+        self.log = [(int(c), str(e)) for c, e in d["log"]]
+        dev = lambda a: torch.as_tensor(a, dtype=like.dtype, device=like.device).reshape(like.shape)
+        self._avg = None if d["avg"] is None else dev(d["avg"]).contiguous()
+        self._avg_spare = None
+        self._avg_grid, self._avg_quad = grid, quad
+        self.diffusivities = None if d["kx"] is None else (dev(d["kx"]).contiguous(),
+                                                           dev(d["ky"]).contiguous())
 
     def scale_average(self, s):
         """psi_avg /= s (R/eigen.py:246-247)."""

@@ -340,3 +340,36 @@ def test_z_fold_matches_full_sphere(P, tag, dtype, tol):
     np.testing.assert_allclose(half.residual_history, full.residual_history, rtol=tol * 10)
     if pd.driver != "fixed_source":
         np.testing.assert_allclose(half.history, full.history, rtol=tol)
+
+
+@pytest.mark.parametrize("tag,dtype,split", [("c2_reduced", "float64", 9),
+                                             ("c2_reduced", "float32", 14),
+                                             ("c3_reduced", "float64", 37)])
+def test_checkpoint_resume_bitwise(P, tmp_path, tag, dtype, split):
+    """Stop after `split` cycles, write a checkpoint, resume in a fresh Solver: the
+    result is bit-identical to the uninterrupted solve (incl. PGState decisions)."""
+    from paper_2301_09991_b200 import benchmarks as B
+    from paper_2301_09991_b200.eigen import Solver
+    from paper_2301_09991_b200.problems import problem_from_data
+    pd = DRIVERS[tag][0](B)
+    o = dict(pd.options)
+    pg = o.pop("pg", None)
+    opts = P.SolverOptions(**o, pg=P.PGConfig(**(pg or {})), dtype=dtype)
+    prob = problem_from_data(pd)
+    inner = pd.inner_iters if pd.driver != "fixed_source" else None
+    ref = Solver(prob, opts, inner).run()
+    a = Solver(prob, opts, inner)
+    for _ in range(split):
+        a.step()
+    path = tmp_path / "ckpt.npz"
+    a.save_checkpoint(path)
+    b = Solver(prob, opts, inner).load_checkpoint(path)
+    res = b.run()
+    assert np.array_equal(res.phi, ref.phi)
+    assert res.residual_history == ref.residual_history
+    assert list(res.pg_log) == list(ref.pg_log)
+    if inner is not None:
+        assert res.history == ref.history
+    with pytest.raises(ValueError):   # signature mismatch
+        Solver(prob, P.SolverOptions(**o, pg=P.PGConfig(**(pg or {})), dtype=dtype,
+                                     fold_z=True), inner).load_checkpoint(path)
