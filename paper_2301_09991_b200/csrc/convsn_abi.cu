@@ -445,7 +445,6 @@ int csn_restrict(int dtype, const csn_geom* gf, const csn_geom* gc, const void* 
     if (gc->na == gf->na) ac = 0;
     else if (gc->na * 2 == gf->na) ac = 1;
     else return CSN_E_ARG;
-    const int64_t total = (int64_t)gc->nx * gc->ny * gc->nd * gc->ng;
     auto run = [&](auto tag) -> int {
         using Real = decltype(tag);
         RestrictArgs<Real> a;
@@ -455,7 +454,15 @@ int csn_restrict(int dtype, const csn_geom* gf, const csn_geom* gc, const void* 
         a.af = (Real)(gf->dx * gf->dy); a.ac = (Real)(gc->dx * gc->dy);
         a.angle_coarsens = ac; a.normalise = normalise;
         a.coarse = (Real*)coarse; a.coarse_h = coarse_halo;
-        restrict_kernel<Real><<<grid1d(total), 256, 0, S(stream)>>>(a);
+        const int64_t cells = (int64_t)gc->nx * gc->ny;
+        if (cells > INT32_MAX) return CSN_E_ARG;
+        // enough CTAs to fill the machine ~8 deep; each strides over coarse cells
+        const int64_t gxc = cdiv((int64_t)gc->nd * gc->ng, 256);
+        int64_t gyc = cdiv(148 * 16, gxc);
+        if (gyc > cells) gyc = cells;
+        if (gyc > 65535) gyc = 65535;
+        if (gyc < 1) gyc = 1;
+        restrict_kernel<Real><<<dim3((unsigned)gxc, (unsigned)gyc), 256, 0, S(stream)>>>(a);
         CSN_CHECK_LAUNCH();
         return CSN_OK;
     };

@@ -19,45 +19,79 @@ struct RestrictArgs {
     Real* coarse; int coarse_h;
 };
 
+// One thread per coarse channel (blockIdx.x * 256 + threadIdx.x), striding over coarse
+// cells with blockIdx.y: the channel decomposition (children, weights, normaliser) is
+// done once per thread, the cell loop is loads + the reference's arithmetic order.  With angle coarsening and
+// ng == 1 the two column children (pb = 0, 1) are adjacent channels: one 8-byte load.
 template <class Real>
 __global__ void __launch_bounds__(256) restrict_kernel(const RestrictArgs<Real> a) {
     const Geo &gf = a.gf, &gc = a.gc;
-    const int64_t total = (int64_t)gc.nx * gc.ny * gc.C;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int cc = (int)(e % gc.C);
-        const int64_t cell = e / gc.C;
-        const int J = (int)(cell % gc.ny), I = (int)(cell / gc.ny);
-        const int N = cc / gc.ng, g = cc - N * gc.ng;
+    const int cc = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cc >= gc.C) return;
+    const int N = cc / gc.ng, g = cc - N * gc.ng;
+    int cf[4];          // fine child channels (pa, pb) = (0,0), (0,1), (1,0), (1,1)
+    Real wn[4];
+    int nch = 1;
+    if (a.angle_coarsens) {
+        const int naf = gf.na, nac = gc.na;
+        const int f = N / (nac * nac), rem = N - f * nac * nac;
+        const int R = rem / nac, Cc = rem - R * nac;
+#pragma unroll
+        for (int pa = 0; pa < 2; ++pa)
+#pragma unroll
+            for (int pb = 0; pb < 2; ++pb) {
+                const int nf = f * naf * naf + (2 * R + pa) * naf + (2 * Cc + pb);
+                cf[pa * 2 + pb] = nf * gf.ng + g;
+                wn[pa * 2 + pb] = a.wf[nf];
+            }
+        nch = 4;
+    } else {
+        cf[0] = cc;
+        wn[0] = a.wf[N];
+    }
+    const Real norm = a.normalise ? a.wc[N] * a.ac : Real(1);
+    const Real af = a.af;
+    const bool pair = nch == 4 && gf.ng == 1;      // cf[1] == cf[0] + 1, cf[0] even
+    const int64_t fpitch = (int64_t)(gf.ny + 2 * a.fine_h) * gf.C;   // x stride (fine)
+    const int ncells = gc.nx * gc.ny;
+    for (int cell = blockIdx.y; cell < ncells; cell += gridDim.y) {
+        const int I = cell / gc.ny, J = cell - I * gc.ny;
+        const Real* f0 = a.fine + fidx(2 * I, 2 * J, 0, gf.ny, a.fine_h, gf.C);
         Real acc = Real(0);
-        if (a.angle_coarsens) {
-            const int naf = gf.na, nac = gc.na;
-            const int f = N / (nac * nac), rem = N - f * nac * nac;
-            const int R = rem / nac, Cc = rem - R * nac;
+        if (pair) {
 #pragma unroll
-            for (int pa = 0; pa < 2; ++pa)
+            for (int pa = 0; pa < 2; ++pa) {
+                Real sp0 = Real(0), sp1 = Real(0);
 #pragma unroll
-                for (int pb = 0; pb < 2; ++pb) {
-                    const int nf = f * naf * naf + (2 * R + pa) * naf + (2 * Cc + pb);
-                    const int cf = nf * gf.ng + g;
-                    const Real wn = a.wf[nf];
-                    Real sp = Real(0);
+                for (int i = 0; i < 2; ++i)
 #pragma unroll
-                    for (int i = 0; i < 2; ++i)
-#pragma unroll
-                        for (int j = 0; j < 2; ++j)
-                            sp += a.fine[fidx(2 * I + i, 2 * J + j, cf, gf.ny, a.fine_h, gf.C)] * wn * a.af;
-                    acc += sp;
-                }
+                    for (int j = 0; j < 2; ++j) {
+                        const Real* q = f0 + i * fpitch + j * gf.C + cf[pa * 2];
+                        Real v0, v1;
+                        if (sizeof(Real) == 4) {
+                            const float2 v = *reinterpret_cast<const float2*>(q);
+                            v0 = (Real)v.x; v1 = (Real)v.y;
+                        } else {
+                            v0 = q[0]; v1 = q[1];
+                        }
+                        sp0 += v0 * wn[pa * 2] * af;
+                        sp1 += v1 * wn[pa * 2 + 1] * af;
+                    }
+                acc += sp0;
+                acc += sp1;
+            }
         } else {
-            const Real wn = a.wf[N];
+            for (int k = 0; k < nch; ++k) {
+                Real sp = Real(0);
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+                for (int i = 0; i < 2; ++i)
 #pragma unroll
-                for (int j = 0; j < 2; ++j)
-                    acc += a.fine[fidx(2 * I + i, 2 * J + j, cc, gf.ny, a.fine_h, gf.C)] * wn * a.af;
+                    for (int j = 0; j < 2; ++j)
+                        sp += f0[i * fpitch + j * gf.C + cf[k]] * wn[k] * af;
+                acc += sp;
+            }
         }
-        if (a.normalise) acc /= a.wc[N] * a.ac;
+        if (a.normalise) acc /= norm;
         a.coarse[fidx(I, J, cc, gc.ny, a.coarse_h, gc.C)] = acc;
     }
 }
