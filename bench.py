@@ -285,7 +285,8 @@ def run_b200(args, rank, world, local_rank):
     esz = 4 if dtype == torch.float32 else 8
     kernel_stats = {}
     for k, ts in probe.items():
-        kernel_stats[k] = {"ms_avg": float(np.mean(ts)), "launches": len(ts)}
+        kernel_stats[k] = {"ms_avg": float(np.mean(ts)), "launches": len(ts),
+                           "ms_min": float(np.min(ts)), "ms_max": float(np.max(ts))}
         if per_dof_bytes(k, esz):
             kernel_stats[k]["GBps"] = per_dof_bytes(k, esz) * dof / (np.mean(ts) * 1e-3) / 1e9
     dominant = "pg_sweep" if "pg_sweep" in probe else "upwind_residual"
