@@ -377,7 +377,12 @@ int csn_apply_boundary(int dtype, const csn_geom* g, void* f, int halo, const vo
     Geo d = make_geo(*g);
     const int64_t cells = (int64_t)2 * halo * (g->ny + 2 * halo) + (int64_t)g->nx * 2 * halo;
     if (cells > INT32_MAX) return CSN_E_ARG;
-    dim3 grid((unsigned)cdiv(d.C, 256), (unsigned)(cells < 65535 ? cells : 65535));
+    // a few CTAs per SM, each looping over halo cells (one cell per CTA is launch-bound)
+    const int64_t gxb = cdiv(d.C, 256);
+    int64_t gyb = cdiv(148 * 8, gxb);
+    if (gyb > cells) gyb = cells;
+    if (gyb > 65535) gyb = 65535;
+    dim3 grid((unsigned)gxb, (unsigned)(gyb < 1 ? 1 : gyb));
     if (dtype == CSN_F32)
         boundary_kernel<float><<<grid, 256, 0, S(stream)>>>(d, (float*)f, halo, (const float*)mu,
                                                             (const float*)nu);
