@@ -382,6 +382,9 @@ class PGState:
                       self._avg.numel(), float(s), 1, _lib.stream())
 
 
+GRAPH_MAX_DOF = 64 * 1024 * 1024
+
+
 class CycleEngine:
     """Device workspaces + kernel sequence of one sawtooth cycle on one hierarchy."""
 
@@ -410,7 +413,10 @@ class CycleEngine:
         self.k_scratch = None
         self.k_work = None         # (key, workspace of the split diffusivity kernels)
         self.probe = None          # {kernel name: [(start event, end event)]} when timing
-        self.use_graphs = True     # replay recurring cycle plans from captured CUDA graphs
+        # replay recurring cycle plans from captured CUDA graphs where the cycle is
+        # launch-bound (small levels); a C4-size cycle (12 ms of kernels) gains nothing
+        # from a graph and would only pay the capture
+        self.use_graphs = shp[0][0] * shp[0][1] * shp[0][2] * shp[0][3] < GRAPH_MAX_DOF
         self._graphs = {}
         self._seen = set()
         self._cap_stream = None
