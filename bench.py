@@ -284,6 +284,7 @@ def run_b200(args, rank, world, local_rank):
     eng.probe = None
     dof = pd.dof() // 2 if args.fold else pd.dof()   # DOF actually updated
     value = dof * args.steps / (ms * 1e-3)          # global DOF: strong scaling over ranks
+    ldof = dof // world                              # this rank's slab: kernel-level rates
 
     # ---- roofline of the dominant kernel (fused PG sweep, K5): 20 B/DOF fp32
     peak, peak_kind, peaks = measured_peaks()
@@ -293,14 +294,16 @@ def run_b200(args, rank, world, local_rank):
         kernel_stats[k] = {"ms_avg": float(np.mean(ts)), "launches": len(ts),
                            "ms_min": float(np.min(ts)), "ms_max": float(np.max(ts))}
         if per_dof_bytes(k, esz):
-            kernel_stats[k]["GBps"] = per_dof_bytes(k, esz) * dof / (np.mean(ts) * 1e-3) / 1e9
+            kernel_stats[k]["GBps"] = per_dof_bytes(k, esz) * ldof / (np.mean(ts) * 1e-3) / 1e9
     dominant = "pg_sweep" if "pg_sweep" in probe else "upwind_residual"
     roof = None
     if dominant in probe:
         ms_k = float(np.mean(probe[dominant]))
-        bpl = per_dof_bytes(dominant, esz) * dof
+        bpl = per_dof_bytes(dominant, esz) * ldof
         achieved = bpl / (ms_k * 1e-3) / 1e9
-        traffic = committed_traffic(args.config, dominant, args.dtype)
+        # the committed ncu capture is of the default 1-GPU workload
+        traffic = (committed_traffic(args.config, dominant, args.dtype)
+                   if world == 1 and not args.fold and args.nx is None else None)
         roof = {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": ("measured (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
@@ -309,7 +312,7 @@ def run_b200(args, rank, world, local_rank):
                 "share_of_step": ms_k * len(probe[dominant]) / (sum(sum(v) for v in probe.values()) or 1),
                 "timing": kernel_timing}
         if pd.options.get("order", 1) >= 3:
-            flops = (32 * (2 * pd.options["order"] + 1) + 22) * dof
+            flops = (32 * (2 * pd.options["order"] + 1) + 22) * ldof
             fp32_peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
             roof["fp32"] = {"tflops": flops / (ms_k * 1e-3) / 1e12, "peak_tflops": fp32_peak,
                             "frac": flops / (ms_k * 1e-3) / 1e12 / fp32_peak,
