@@ -57,6 +57,16 @@ int csn_version(void);
 /* Kernels this library has launched since it was loaded (instrumentation). */
 unsigned long long csn_launch_count(void);
 const char* csn_error_string(int code);
+/* Kernel-variant switches (no reference counterpart; used by the A/B parity tests):
+ *   "upwind_x2"  = 1 (default): csn_upwind_smooth takes the packed channel-pair kernel
+ *                  where it applies; 0 forces the scalar kernel (bit-identical results);
+ *   "upwind_div" = 2 (default): fp32 smoother forms r / d as the reciprocal product
+ *                  refined by one residual step (the rounded quotient), then subtracts;
+ *                  1: IEEE division; 0: one fused ce - r * rcp(d) (less accurate);
+ *   "sweep_div"  = 1 (default): the fp32 PG sweep refines r / (beta d) the same way;
+ *                  0: reciprocal product.
+ * The previous value is stored in *prev (nullable). */
+int csn_set_tuning(const char* key, int value, int* prev);
 
 /* Doubles of workspace a reduction-producing call needs for its per-block partials. */
 int64_t csn_partials_size(int dtype, const csn_geom* g, int order);

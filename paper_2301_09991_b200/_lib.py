@@ -33,6 +33,7 @@ _SIGNATURES = {
     "csn_version": ([], _c_int),
     "csn_launch_count": ([], ctypes.c_ulonglong),
     "csn_error_string": ([_c_int], ctypes.c_char_p),
+    "csn_set_tuning": ([ctypes.c_char_p, _c_int, ctypes.POINTER(ctypes.c_int)], _c_int),
     "csn_partials_size": ([_c_int, _GP, _c_int], _c_i64),
     "csn_apply_boundary": ([_c_int, _GP, _vp, _c_int, _vp, _vp, _vp], _c_int),
     "csn_upwind_residual": ([_c_int, _GP, _vp, _c_int, _vp, _vp, _c_int, _vp, _vp, _vp, _c_int,
@@ -96,6 +97,14 @@ def check(code, what):
 
 def call(name, *args):
     check(getattr(load(), name)(*args), name)
+
+
+def set_tuning(key, value):
+    """Switch a kernel variant (csn_set_tuning); returns the previous value."""
+    prev = ctypes.c_int(0)
+    check(load().csn_set_tuning(key.encode(), int(value), ctypes.byref(prev)),
+          f"csn_set_tuning({key!r})")
+    return prev.value
 
 
 def require_cuda(t, what="field"):

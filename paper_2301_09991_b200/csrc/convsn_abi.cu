@@ -15,6 +15,11 @@ unsigned long long csn::g_launches = 0;
 
 namespace {
 
+// kernel-variant switches (csn_set_tuning), for A/B parity tests of kernel variants
+int g_tune_upwind_x2 = 1;
+int g_tune_upwind_div = 2;
+int g_tune_sweep_div = 1;
+
 constexpr int kVersion = 1;
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -148,6 +153,7 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
     a.hx = (Real)(0.5 / (g->dx * g->dx)); a.hy = (Real)(0.5 / (g->dy * g->dy));
     a.r = (Real*)r; a.r_h = r_h;
     a.out = (Real*)out; a.out_h = out_h; a.beta = (Real)beta;
+    a.refine_div = g_tune_sweep_div;
     // fp32: packed-fp32x2 kernel, a lane per channel pair (64 channels per CTA)
     constexpr bool X2 = sizeof(Real) == 4;
     const int gx = (int)cdiv(g->nx, PG_TX);
@@ -315,6 +321,41 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
     a.inv_dx = (Real)(1.0 / g->dx); a.inv_dy = (Real)(1.0 / g->dy);
     a.scale = (Real)diag_scale; a.use_scale = diag_scale != 1.0;
     a.out = (Real*)out; a.out_h = out_h;
+    a.exact_div = g_tune_upwind_div;
+    if constexpr (std::is_same<Real, float>::value) {
+        // packed channel-pair kernel when a 64-channel CTA lies in one face (see
+        // upwind_smooth_x2_kernel); the scalar kernel covers every other case
+        const int64_t C = (int64_t)g->nd * g->ng;
+        const int64_t face = (int64_t)g->na * g->na * g->ng;
+        const bool g1 = g->ng == 1;
+        if (g_tune_upwind_x2 && n_sweeps == 3 && q_per_dof && C % UPX_CC == 0 &&
+            face % UPX_CC == 0 && (g1 || g->ng % 2 == 0) &&
+            !(g1 && init_mode == 2 && !a.angle_coarsens)) {
+            const int gx = (int)cdiv(cdiv(g->ny, UPX_UT), UPX_SPB);
+            const int gy = (int)(C / UPX_CC);
+            int chunks = (int)cdiv(g->nx, UP_XCHUNK);
+            while (chunks > 1 && (int64_t)gx * gy * (chunks / 2) >= 148 * 8) chunks /= 2;
+            a.xchunk = (int)cdiv(g->nx, chunks);
+            const int gz = (int)cdiv(g->nx, a.xchunk);
+            dim3 grid(gx, gy, gz), block(32, UPX_SPB);
+            auto go = [&](auto g1t, auto dmt) {
+                upwind_smooth_x2_kernel<3, decltype(g1t)::value, decltype(dmt)::value>
+                    <<<grid, block, 0, st>>>(a);
+            };
+            using T_ = std::true_type;
+            using F_ = std::false_type;
+            using D0 = std::integral_constant<int, 0>;
+            using D1 = std::integral_constant<int, 1>;
+            using D2 = std::integral_constant<int, 2>;
+            if (g1) {
+                if (a.exact_div == 2) go(T_(), D2()); else if (a.exact_div) go(T_(), D1()); else go(T_(), D0());
+            } else {
+                if (a.exact_div == 2) go(F_(), D2()); else if (a.exact_div) go(F_(), D1()); else go(F_(), D0());
+            }
+            CSN_CHECK_LAUNCH();
+            return CSN_OK;
+        }
+    }
     const int gx = (int)cdiv(cdiv(g->ny, UT), UP_SPB);
     const int gy = (int)cdiv((int64_t)g->nd * g->ng, UP_CC);
     // x chunks: keep chunks long against the H-column warm-up, fill the machine
@@ -344,6 +385,18 @@ extern "C" {
 int csn_version(void) { return kVersion; }
 
 unsigned long long csn_launch_count(void) { return g_launches; }
+
+int csn_set_tuning(const char* key, int value, int* prev) {
+    if (!key) return CSN_E_ARG;
+    int* slot = nullptr;
+    if (!strcmp(key, "upwind_x2")) slot = &g_tune_upwind_x2;
+    if (!strcmp(key, "upwind_div")) slot = &g_tune_upwind_div;
+    if (!strcmp(key, "sweep_div")) slot = &g_tune_sweep_div;
+    if (!slot) return CSN_E_ARG;
+    if (prev) *prev = *slot;
+    *slot = value;
+    return CSN_OK;
+}
 
 const char* csn_error_string(int code) {
     switch (code) {

@@ -67,6 +67,7 @@ struct PGResidArgs {
     double* partials;
     Real* avg; int avg_h; int avg_mode; Real theta, omt;   // fused EMA (frozen cycles)
     int ly;             // y rows per CTA chunk, multiple of T
+    int refine_div;     // fp32 sweep: refine r / (beta d) to the rounded quotient
 };
 
 // residual kernel modes: plain residual, residual + fused iterate EMA, fused sweep

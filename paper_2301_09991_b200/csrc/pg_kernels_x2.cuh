@@ -211,7 +211,10 @@ pg_residual_x2_kernel(const PGResidArgs<float> a) {
             if (SWEEP) {                                                              \
                 const float2 d_ = mul2(beta2, add2(strm2, sg_));                      \
                 const float2 inv_ = make_float2(rcp_nr(d_.x), rcp_nr(d_.y));          \
-                st2(o_p + (int64_t)y_ * g.C, sub2(pc_, mul2(r_, inv_)));             \
+                float2 qt_ = mul2(r_, inv_);                                          \
+                if (a.refine_div)                                                     \
+                    qt_ = fma2(fma2(make_float2(-d_.x, -d_.y), qt_, r_), inv_, qt_);  \
+                st2(o_p + (int64_t)y_ * g.C, sub2(pc_, qt_));                         \
             } else {                                                                  \
                 if (o_p) st2(o_p + (int64_t)y_ * g.C, r_);                           \
                 l1 += fabs((double)r_.x) + fabs((double)r_.y);                        \
