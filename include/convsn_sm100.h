@@ -60,9 +60,12 @@ const char* csn_error_string(int code);
 /* Kernel-variant switches (no reference counterpart; used by the A/B parity tests):
  *   "upwind_x2"  = 1 (default): csn_upwind_smooth takes the packed channel-pair kernel
  *                  where it applies; 0 forces the scalar kernel (bit-identical results);
- *   "upwind_div" = 2 (default): fp32 smoother forms r / d as the reciprocal product
- *                  refined by one residual step (the rounded quotient), then subtracts;
- *                  1: IEEE division; 0: one fused ce - r * rcp(d) (less accurate);
+ *   "upwind_div" = 3 (default): fp32 smoother in Jacobi form, new = (1 - 1/s) ce +
+ *                  b / (s d) with b = the upwind neighbour terms + source, the quotient
+ *                  refined by one residual step (the rounded quotient); 4: the same
+ *                  without refinement; 2: ce - r / (s d) with the refined quotient;
+ *                  1: ce - r / (s d) by IEEE division; 0: one fused ce - r * rcp(s d).
+ *                  fp64 always uses the reference form ce - r / (s d).
  *   "sweep_div"  = 1 (default): the fp32 PG sweep refines r / (beta d) the same way;
  *                  0: reciprocal product.
  * The previous value is stored in *prev (nullable). */

@@ -8,6 +8,7 @@
 #include "pg_kernels.cuh"
 #include "pg_kernels_x2.cuh"
 #include "upwind_kernels.cuh"
+#include "launchers.h"
 
 using namespace csn;
 
@@ -17,7 +18,7 @@ namespace {
 
 // kernel-variant switches (csn_set_tuning), for A/B parity tests of kernel variants
 int g_tune_upwind_x2 = 1;
-int g_tune_upwind_div = 2;
+int g_tune_upwind_div = 3;
 int g_tune_sweep_div = 1;
 
 constexpr int kVersion = 1;
@@ -59,11 +60,6 @@ bool taps_match(const double* taps) {
     return true;
 }
 
-template <class K>
-void set_smem(K kernel, size_t bytes) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-}
-
 // 16-byte staging needs every aligned VEC-channel group inside one octahedron face
 // (same upwind signs) and VEC | C (alignment): a face holds n_a^2 * ng channels
 // (8 faces, or 4 for the z-folded hemisphere).
@@ -73,59 +69,9 @@ inline bool vec_ok(const csn_geom* g, int vec) {
     return C % vec == 0 && face % vec == 0 && C % face == 0;
 }
 
-template <class Real, int L, int MODE, int VEC>
-void launch_pg_resid(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<Real>& a) {
-    constexpr size_t sm = pg_residual_smem<Real, L, MODE>();
-    static bool attr = false;
-    if (!attr) { set_smem(pg_residual_kernel<Real, L, MODE, VEC>, sm); attr = true; }
-    pg_residual_kernel<Real, L, MODE, VEC><<<grid, block, sm, st>>>(a);
-}
-
-template <int L, int MODE, int VEC>
-void launch_pg_resid_x2(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<float>& a) {
-    constexpr size_t sm = pg_residual_x2_smem<L, MODE>();
-    static bool attr = false;
-    if (!attr) { set_smem(pg_residual_x2_kernel<L, MODE, VEC>, sm); attr = true; }
-    pg_residual_x2_kernel<L, MODE, VEC><<<grid, block, sm, st>>>(a);
-}
-
-template <int L, bool EMA, int VEC>
-void launch_pg_k_x2(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a) {
-    constexpr size_t sm = pg_k_x2_smem<L, EMA>();
-    static bool attr = false;
-    if (!attr) { set_smem(pg_diffusivity_x2_kernel<L, EMA, VEC>, sm); attr = true; }
-    pg_diffusivity_x2_kernel<L, EMA, VEC><<<grid, block, sm, st>>>(a);
-}
-
-template <int L, bool EMA, int VEC>
-void launch_pg_grad_x2(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a, float* gx,
-                       float* gy, int gh) {
-    constexpr size_t sm = pg_grad_x2_smem<L, EMA>();
-    static bool attr = false;
-    if (!attr) { set_smem(pg_grad_x2_kernel<L, EMA, VEC>, sm); attr = true; }
-    pg_grad_x2_kernel<L, EMA, VEC><<<grid, block, sm, st>>>(a, gx, gy, gh);
-}
-
-template <int L, int VEC>
-void launch_pg_kcoef_x2(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a,
-                        const float* gx, const float* gy, int gh) {
-    constexpr size_t sm = pg_kcoef_x2_smem<L>();
-    static bool attr = false;
-    if (!attr) { set_smem(pg_kcoef_x2_kernel<L, VEC>, sm); attr = true; }
-    pg_kcoef_x2_kernel<L, VEC><<<grid, block, sm, st>>>(a, gx, gy, gh);
-}
-
 // workspace of the split diffusivity path: psi_x, psi_y on the +-2l band (halo 2l)
 inline int64_t grad_field_elems(const csn_geom* g, int L) {
     return (int64_t)(g->nx + 4 * L) * (g->ny + 4 * L) * g->nd * g->ng;
-}
-
-template <class Real, int L, bool EMA, int VEC>
-void launch_pg_k(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<Real>& a) {
-    constexpr size_t sm = pg_k_smem<Real, L, EMA>();
-    static bool attr = false;
-    if (!attr) { set_smem(pg_diffusivity_kernel<Real, L, EMA, VEC>, sm); attr = true; }
-    pg_diffusivity_kernel<Real, L, EMA, VEC><<<grid, block, sm, st>>>(a);
 }
 
 // ------------------------------------------------------------------ PG residual
@@ -184,7 +130,7 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
             CSN_CHECK_LAUNCH();
         }
         return CSN_OK;
-    }
+    } else {
     if (out) {
         if (vec) launch_pg_resid<Real, L, PG_SWEEP, V>(grid, block, st, a);
         else launch_pg_resid<Real, L, PG_SWEEP, 1>(grid, block, st, a);
@@ -205,6 +151,7 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
         }
     }
     return CSN_OK;
+    }
 }
 
 template <class Real, int L>
@@ -280,7 +227,7 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
         CSN_CHECK_LAUNCH();
         return CSN_OK;
       }
-    }
+    } else {
     const int gx = (int)cdiv(g->nx + 2 * L, TXO);
     const int gy = (int)cdiv((int64_t)g->nd * g->ng, PG_CC);
     a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T);
@@ -295,6 +242,7 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
     }
     CSN_CHECK_LAUNCH();
     return CSN_OK;
+    }
 }
 
 template <class Real>
@@ -321,7 +269,8 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
     a.inv_dx = (Real)(1.0 / g->dx); a.inv_dy = (Real)(1.0 / g->dy);
     a.scale = (Real)diag_scale; a.use_scale = diag_scale != 1.0;
     a.out = (Real*)out; a.out_h = out_h;
-    a.exact_div = g_tune_upwind_div;
+    a.exact_div = std::is_same<Real, float>::value ? g_tune_upwind_div : 0;   // fp64: r / d
+    a.keep = (Real)(1.0 - 1.0 / diag_scale);
     if constexpr (std::is_same<Real, float>::value) {
         // packed channel-pair kernel when a 64-channel CTA lies in one face (see
         // upwind_smooth_x2_kernel); the scalar kernel covers every other case
@@ -347,11 +296,18 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
             using D0 = std::integral_constant<int, 0>;
             using D1 = std::integral_constant<int, 1>;
             using D2 = std::integral_constant<int, 2>;
-            if (g1) {
-                if (a.exact_div == 2) go(T_(), D2()); else if (a.exact_div) go(T_(), D1()); else go(T_(), D0());
-            } else {
-                if (a.exact_div == 2) go(F_(), D2()); else if (a.exact_div) go(F_(), D1()); else go(F_(), D0());
-            }
+            using D3 = std::integral_constant<int, 3>;
+            using D4 = std::integral_constant<int, 4>;
+            auto pick = [&](auto g1t) {
+                switch (a.exact_div) {
+                    case 0: go(g1t, D0()); break;
+                    case 1: go(g1t, D1()); break;
+                    case 2: go(g1t, D2()); break;
+                    case 3: go(g1t, D3()); break;
+                    default: go(g1t, D4()); break;
+                }
+            };
+            if (g1) pick(T_()); else pick(F_());
             CSN_CHECK_LAUNCH();
             return CSN_OK;
         }

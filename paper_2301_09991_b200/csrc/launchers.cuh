@@ -1,0 +1,63 @@
+// Definitions of the PG kernel launchers (launchers.h); included by pg_part.cu only.
+#pragma once
+#include "launchers.h"
+#include "pg_kernels_x2.cuh"
+
+namespace csn {
+
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <class Real, int L, int MODE, int VEC>
+void launch_pg_resid(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<Real>& a) {
+    constexpr size_t sm = pg_residual_smem<Real, L, MODE>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_residual_kernel<Real, L, MODE, VEC>, sm); attr = true; }
+    pg_residual_kernel<Real, L, MODE, VEC><<<grid, block, sm, st>>>(a);
+}
+
+template <int L, int MODE, int VEC>
+void launch_pg_resid_x2(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<float>& a) {
+    constexpr size_t sm = pg_residual_x2_smem<L, MODE>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_residual_x2_kernel<L, MODE, VEC>, sm); attr = true; }
+    pg_residual_x2_kernel<L, MODE, VEC><<<grid, block, sm, st>>>(a);
+}
+
+template <int L, bool EMA, int VEC>
+void launch_pg_k_x2(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a) {
+    constexpr size_t sm = pg_k_x2_smem<L, EMA>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_diffusivity_x2_kernel<L, EMA, VEC>, sm); attr = true; }
+    pg_diffusivity_x2_kernel<L, EMA, VEC><<<grid, block, sm, st>>>(a);
+}
+
+template <int L, bool EMA, int VEC>
+void launch_pg_grad_x2(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a, float* gx,
+                       float* gy, int gh) {
+    constexpr size_t sm = pg_grad_x2_smem<L, EMA>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_grad_x2_kernel<L, EMA, VEC>, sm); attr = true; }
+    pg_grad_x2_kernel<L, EMA, VEC><<<grid, block, sm, st>>>(a, gx, gy, gh);
+}
+
+template <int L, int VEC>
+void launch_pg_kcoef_x2(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a,
+                        const float* gx, const float* gy, int gh) {
+    constexpr size_t sm = pg_kcoef_x2_smem<L>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_kcoef_x2_kernel<L, VEC>, sm); attr = true; }
+    pg_kcoef_x2_kernel<L, VEC><<<grid, block, sm, st>>>(a, gx, gy, gh);
+}
+
+template <class Real, int L, bool EMA, int VEC>
+void launch_pg_k(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<Real>& a) {
+    constexpr size_t sm = pg_k_smem<Real, L, EMA>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_diffusivity_kernel<Real, L, EMA, VEC>, sm); attr = true; }
+    pg_diffusivity_kernel<Real, L, EMA, VEC><<<grid, block, sm, st>>>(a);
+}
+
+}  // namespace csn
