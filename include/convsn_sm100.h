@@ -67,7 +67,9 @@ const char* csn_error_string(int code);
  *                  1: ce - r / (s d) by IEEE division; 0: one fused ce - r * rcp(s d).
  *                  fp64 always uses the reference form ce - r / (s d).
  *   "sweep_div"  = 1 (default): the fp32 PG sweep refines r / (beta d) the same way;
- *                  0: reciprocal product.
+ *                  0: reciprocal product;
+ *   "pg_tma"     = 1 (default): fp32 csn_pg_residual stages padded fields with TMA
+ *                  (mbarrier ring); 0 forces the cp.async kernel (bit-identical).
  * The previous value is stored in *prev (nullable). */
 int csn_set_tuning(const char* key, int value, int* prev);
 
@@ -142,7 +144,12 @@ int64_t csn_pg_workspace_size(int dtype, const csn_geom* g, int order);
  *   sweep    (psi_out != NULL): R/multigrid.py:301-304 fused — psi' = psi - delta
  *            (delta nullable), psi_out = psi' - pg_residual(psi') / (beta (|mu|/dx + |nu|/dy
  *            + sigma)) (R/multigrid.py:159-172).  psi_out must not alias psi.
- * strm: device [nd] = |mu|/dx + |nu|/dy. */
+ * strm: device [nd] = |mu|/dx + |nu|/dy.
+ * Halos: like the reference (which evaluates psi.data with its stored halo), the caller
+ * applies the boundary first (csn_apply_boundary; R/multigrid.py:166,277) and kx, ky are
+ * zero outside their +-l band.  fp32 fields padded by >= l (delta too, in the sweep) are
+ * staged with TMA as stored; otherwise the kernel re-derives the halo by the vacuum rule
+ * — identical for consistent halos (tests/test_gpu_parity.py, tma_residual). */
 int csn_pg_residual(int dtype, int order, const csn_geom* g, const double* taps,
                     const void* psi, int psi_halo, const void* delta, int delta_halo,
                     const void* kx, const void* ky, int k_halo,

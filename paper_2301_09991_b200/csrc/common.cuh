@@ -165,6 +165,15 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// iterate average pbar' = (1 - theta) pbar + theta psi (R/multigrid.py:217-225) with a
+// fixed contraction, so every kernel that forms it rounds identically
+__device__ __forceinline__ float ema_rn(float b, float p, float omt, float th) {
+    return __fmaf_rn(b, omt, __fmul_rn(th, p));
+}
+__device__ __forceinline__ double ema_rn(double b, double p, double omt, double th) {
+    return __fma_rn(b, omt, __dmul_rn(th, p));
+}
+
 // NaN-propagating min (numpy.minimum semantics, R/discretisation.py:150-158).
 template <class Real>
 __device__ __forceinline__ Real nanmin(Real a, Real b) {

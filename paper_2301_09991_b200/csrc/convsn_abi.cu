@@ -1,5 +1,7 @@
 // extern "C" entry points of libconvsn_sm100.so (declared in include/convsn_sm100.h).
 // Argument checking, launch geometry and float/double x ConvFEM-order dispatch.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <math.h>
 #include <string.h>
 
@@ -8,6 +10,7 @@
 #include "pg_kernels.cuh"
 #include "pg_kernels_x2.cuh"
 #include "upwind_kernels.cuh"
+#include "pg_kernels_tma.cuh"
 #include "launchers.h"
 
 using namespace csn;
@@ -20,6 +23,41 @@ namespace {
 int g_tune_upwind_x2 = 1;
 int g_tune_upwind_div = 3;
 int g_tune_sweep_div = 1;
+int g_tune_pg_tma = 1;
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        else
+            cudaGetLastError();
+    }
+    return fn;
+}
+
+// 3D map over a padded fp32 field [nx + 2h][ny + 2h][C]: box = 64 channels x 1 row x bx
+// cells, out-of-bounds boxes zero-filled, 256-byte L2 promotion
+bool field_map(CUtensorMap* m, const void* base, const csn_geom* g, int h, int bx) {
+    auto enc = tensor_map_encoder();
+    if (!enc || !base) return false;
+    const uint64_t C = (uint64_t)g->nd * g->ng;
+    if ((C * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+    cuuint64_t dims[3] = {C, (cuuint64_t)(g->ny + 2 * h), (cuuint64_t)(g->nx + 2 * h)};
+    cuuint64_t strides[2] = {C * 4, (cuuint64_t)(g->ny + 2 * h) * C * 4};
+    cuuint32_t box[3] = {64, 1, (cuuint32_t)bx};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box,
+               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+}
 
 constexpr int kVersion = 1;
 
@@ -111,6 +149,28 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
     const bool vec = vec_ok(g, 16 / (int)sizeof(Real));
     constexpr int V = 16 / sizeof(Real);
     if constexpr (X2) {
+        // TMA staging when every staged field is padded (halos read as stored)
+        constexpr int W = PG_TX + 2 * L;
+        PGTmaMaps maps;
+        const bool tma = g_tune_pg_tma && psi_h >= L && k_h >= L &&
+                         (!out || (delta && delta_h >= L)) &&
+                         field_map(&maps.psi, psi, g, psi_h, W) &&
+                         field_map(&maps.kx, kx, g, k_h, W) && field_map(&maps.ky, ky, g, k_h, W) &&
+                         (out ? field_map(&maps.aux, delta, g, delta_h, W)
+                              : (!a.avg_mode || field_map(&maps.aux, avg, g, avg_h, PG_TX)));
+        if (!tma) cudaGetLastError();
+        if (tma) {
+            if (!out && l1 && !partials) return CSN_E_ARG;
+            if (out) launch_pg_resid_tma<L, PG_SWEEP>(grid, block, st, a, maps);
+            else if (a.avg_mode) launch_pg_resid_tma<L, PG_RESID_EMA>(grid, block, st, a, maps);
+            else launch_pg_resid_tma<L, PG_RESID>(grid, block, st, a, maps);
+            CSN_CHECK_LAUNCH();
+            if (!out && l1) {
+                sum_f64_kernel<<<1, 1024, 0, st>>>(partials, (int64_t)gx * gy * gz, 1.0, l1);
+                CSN_CHECK_LAUNCH();
+            }
+            return CSN_OK;
+        }
         if (out) {
             if (vec) launch_pg_resid_x2<L, PG_SWEEP, V>(grid, block, st, a);
             else launch_pg_resid_x2<L, PG_SWEEP, 1>(grid, block, st, a);
@@ -348,6 +408,7 @@ int csn_set_tuning(const char* key, int value, int* prev) {
     if (!strcmp(key, "upwind_x2")) slot = &g_tune_upwind_x2;
     if (!strcmp(key, "upwind_div")) slot = &g_tune_upwind_div;
     if (!strcmp(key, "sweep_div")) slot = &g_tune_sweep_div;
+    if (!strcmp(key, "pg_tma")) slot = &g_tune_pg_tma;
     if (!slot) return CSN_E_ARG;
     if (prev) *prev = *slot;
     *slot = value;

@@ -7,11 +7,18 @@
 #include "pg_kernels.cuh"
 
 namespace csn {
+struct PGTmaMaps;
+}
+
+namespace csn {
 
 template <class Real, int L, int MODE, int VEC>
 void launch_pg_resid(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<Real>& a);
 template <int L, int MODE, int VEC>
 void launch_pg_resid_x2(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<float>& a);
+template <int L, int MODE>
+void launch_pg_resid_tma(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<float>& a,
+                         const PGTmaMaps& maps);
 template <int L, bool EMA, int VEC>
 void launch_pg_k_x2(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a);
 template <int L, bool EMA, int VEC>

@@ -9,6 +9,15 @@ namespace csn {
 // ------------------------------------------------------------------ restriction
 // s_c[I,J,N] = sum_{2x2 cells} sum_{children n of N} r[i,j,n] w_n dxf dyf  (raw),
 // divided by w_N dxc dyc when normalise (R/multigrid.py:326).
+// explicitly rounded products / sums (no contraction), shared with the restriction
+// fused into the fp32 residual kernel (pg_residual_x2_kernel<..., RC = true>)
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+
 template <class Real>
 struct RestrictArgs {
     Geo gf, gc;
@@ -49,7 +58,8 @@ __global__ void __launch_bounds__(256) restrict_kernel(const RestrictArgs<Real> 
         cf[0] = cc;
         wn[0] = a.wf[N];
     }
-    const Real norm = a.normalise ? a.wc[N] * a.ac : Real(1);
+    // 1 / (w_N ac) once per channel (the fused restriction uses the same product)
+    const Real inorm = a.normalise ? div_rn(Real(1), mul_rn(a.wc[N], a.ac)) : Real(1);
     const Real af = a.af;
     const bool pair = nch == 4 && gf.ng == 1;      // cf[1] == cf[0] + 1, cf[0] even
     const int64_t fpitch = (int64_t)(gf.ny + 2 * a.fine_h) * gf.C;   // x stride (fine)
@@ -74,11 +84,11 @@ __global__ void __launch_bounds__(256) restrict_kernel(const RestrictArgs<Real> 
                         } else {
                             v0 = q[0]; v1 = q[1];
                         }
-                        sp0 += v0 * wn[pa * 2] * af;
-                        sp1 += v1 * wn[pa * 2 + 1] * af;
+                        sp0 = add_rn(sp0, mul_rn(mul_rn(v0, wn[pa * 2]), af));
+                        sp1 = add_rn(sp1, mul_rn(mul_rn(v1, wn[pa * 2 + 1]), af));
                     }
-                acc += sp0;
-                acc += sp1;
+                acc = add_rn(acc, sp0);
+                acc = add_rn(acc, sp1);
             }
         } else {
             for (int k = 0; k < nch; ++k) {
@@ -87,11 +97,11 @@ __global__ void __launch_bounds__(256) restrict_kernel(const RestrictArgs<Real> 
                 for (int i = 0; i < 2; ++i)
 #pragma unroll
                     for (int j = 0; j < 2; ++j)
-                        sp += f0[i * fpitch + j * gf.C + cf[k]] * wn[k] * af;
-                acc += sp;
+                        sp = add_rn(sp, mul_rn(mul_rn(f0[i * fpitch + j * gf.C + cf[k]], wn[k]), af));
+                acc = add_rn(acc, sp);
             }
         }
-        if (a.normalise) acc /= norm;
+        if (a.normalise) acc = mul_rn(acc, inorm);
         a.coarse[fidx(I, J, cc, gc.ny, a.coarse_h, gc.C)] = acc;
     }
 }
@@ -275,7 +285,7 @@ ema_kernel(Geo g, Real* avg, int ah, const Real* psi, int ph, Real theta, Real o
         const int y = (int)(cell % g.ny), x = (int)(cell / g.ny);
         const Real p = psi[fidx(x, y, c, g.ny, ph, g.C)];
         Real* o = avg + fidx(x, y, c, g.ny, ah, g.C);
-        *o = mode == 1 ? p : *o * omt + theta * p;
+        *o = mode == 1 ? p : ema_rn(*o, p, omt, theta);
     }
 }
 

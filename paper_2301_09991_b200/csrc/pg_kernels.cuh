@@ -175,7 +175,7 @@ pg_residual_kernel(const PGResidArgs<Real> a) {
                         const Real* p_ = buf_ + (e / G4) * PG_CC + (e % G4) * VEC;   \
                         Real* o_ = avg_p[i] + (int64_t)yl_ * g.C;                    \
                         _Pragma("unroll") for (int v = 0; v < VEC; ++v)              \
-                            o_[v] = a.avg_mode == 2 ? p_[3 * FS + v] * a.omt + a.theta * p_[v] \
+                            o_[v] = a.avg_mode == 2 ? ema_rn(p_[3 * FS + v], p_[v], a.omt, a.theta) \
                                                     : p_[v];                         \
                     }                                                                \
                 }                                                                    \
@@ -396,7 +396,7 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
 #pragma unroll
                         for (int vv = 0; vv < VEC; ++vv) {
                             pv[vv] = p[vv];
-                            if (EMA) pv[vv] = p[FS + vv] * omt + theta * pv[vv];
+                            if (EMA) pv[vv] = ema_rn(p[FS + vv], pv[vv], omt, theta);
                             p[vv] = pv[vv];
                         }
                         if (own_ptr[i] && own_row) {

@@ -1,0 +1,282 @@
+// fp32 PG residual / fused sweep (K3 / K3E / K5) with TMA row staging and an mbarrier
+// producer/consumer ring (sm_100a).
+//
+// Same operator, lane mapping (channel pairs, FFMA2) and arithmetic as
+// pg_residual_x2_kernel — results are bit-identical — with the staging re-done the
+// Blackwell way:
+//   * one elected thread stages a whole cell row of every field with
+//     cp.async.bulk.tensor (TMA, a 3D tensor map over the padded [x][y][channel]
+//     field, box = W cells x 1 row x 64 channels); no per-thread address / vacuum-rule
+//     math, no per-thread LDGSTS;
+//   * slot readiness is an mbarrier with a transaction count (full[s]); slot reuse is
+//     a second mbarrier that each warp arrives on after its last read of the row
+//     (empty[s], 8 arrivals).  There is no CTA-wide barrier in the march: a warp only
+//     waits for data, so warps drift up to P rows apart instead of lock-stepping.
+// Halos are read AS STORED, like the reference's pg_residual (R/discretisation.py:
+// 239-276 works on psi.data with its stored halo): the caller applies the boundary
+// first (sawtooth_cycle does, R/multigrid.py:166,277,305) and k is zero outside its
+// band.  The sweep's psi' = psi - delta is formed at each read (delta padded by >= L
+// with its boundary applied); the frozen-cycle iterate average reads pbar_old through
+// a second (8-cell) box and writes pbar from the consuming thread.
+#pragma once
+#include <cuda.h>
+
+#include "pg_kernels_x2.cuh"
+
+namespace csn {
+
+struct PGTmaMaps {
+    CUtensorMap psi, kx, ky, aux;   // aux: delta (sweep) or pbar_old (EMA)
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "MBW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra MBW_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int L, int MODE>
+constexpr size_t pg_residual_tma_smem() {
+    return (size_t)X2Stages<L>::value * (MODE == PG_RESID ? 3 : 4) * (PG_TX + 2 * L) * X2_CC *
+               sizeof(float) + 128;   // + alignment slack (TMA destinations: 128 B)
+}
+
+template <int L, int MODE>
+__global__ void __launch_bounds__(32 * PG_TX, L <= 3 ? 2 : 1)
+pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTmaMaps m) {
+    constexpr bool SWEEP = MODE == PG_SWEEP;
+    constexpr bool EMA = MODE == PG_RESID_EMA;
+    using TP = UnitTaps<L>;
+    constexpr int T = 2 * L + 1;
+    constexpr int CC = X2_CC;
+    constexpr int W = PG_TX + 2 * L;
+    constexpr int NF = MODE == PG_RESID ? 3 : 4;
+    constexpr int S = X2Stages<L>::value;
+    constexpr int P = S - L - 1;
+    constexpr int FS = W * CC;                     // floats per field row
+    constexpr unsigned ROWB = W * CC * sizeof(float);
+    constexpr unsigned TXB = 3 * ROWB + (SWEEP ? ROWB : 0) + (EMA ? PG_TX * CC * sizeof(float) : 0);
+    extern __shared__ unsigned char smraw[];
+    float* sm = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+    __shared__ double red[32];
+    __shared__ __align__(8) uint64_t full[S], empty[S];
+
+    const Geo& g = a.g;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = ty * 32 + tx;
+    const int c0 = blockIdx.y * CC;
+    const int c = c0 + 2 * tx;                     // C = n_dir * n_group is even
+    const bool cval = c < g.C;
+    const int cs = cval ? c : g.C - 2;
+    const int n0 = cs / g.ng, g0 = cs - n0 * g.ng;
+    const int n1 = (cs + 1) / g.ng, g1 = cs + 1 - n1 * g.ng;
+    const float2 mu_dx = make_float2(a.mu[n0] * a.inv_dx, a.mu[n1] * a.inv_dx);
+    const float2 nu_dy = make_float2(a.nu[n0] * a.inv_dy, a.nu[n1] * a.inv_dy);
+    const float2 hx = bc2(a.hx), hy = bc2(a.hy), mhx = bc2(-a.hx), mhy = bc2(-a.hy);
+    const int x0 = blockIdx.x * PG_TX;
+    const int x = x0 + ty;
+    const int ya = blockIdx.z * a.ly;
+    const int yb = min(g.ny, ya + a.ly);
+    const bool act = x < g.nx && cval;
+    const int nsteps = 2 * L + (int)(((yb - ya) + T - 1) / T) * T;   // lead rows ya-L ...
+    const bool producer = tid == 0;
+
+    if (producer) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], PG_TX);           // one arrival per warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    // producer: lead row ya - L + k of every field into slot s
+    auto issue = [&](int k, int s) {
+        const int yy = ya - L + k;
+        float* dst = sm + s * (NF * FS);
+        mbar_expect_tx(&full[s], TXB);
+        tma_load_3d(dst, &m.psi, &full[s], c0, yy + a.psi_h, x0 - L + a.psi_h);
+        tma_load_3d(dst + FS, &m.kx, &full[s], c0, yy + a.k_h, x0 - L + a.k_h);
+        tma_load_3d(dst + 2 * FS, &m.ky, &full[s], c0, yy + a.k_h, x0 - L + a.k_h);
+        if (SWEEP) tma_load_3d(dst + 3 * FS, &m.aux, &full[s], c0, yy + a.delta_h, x0 - L + a.delta_h);
+        if (EMA) tma_load_3d(dst + 3 * FS, &m.aux, &full[s], c0, yy + a.avg_h, x0 + a.avg_h);
+    };
+
+    // epilogue pointers at y = 0 (per output only y * stride is added)
+    const int xs = act ? x : 0;
+    const int64_t cell0 = (int64_t)xs * g.ny;
+    const float* sig0 = a.sigma + cell0 * g.ng + g0;
+    const float* sig1 = a.sigma + cell0 * g.ng + g1;
+    const int qst = a.q_per_dof ? g.C : g.ng;
+    const float* q0 = a.q + cell0 * qst + (a.q_per_dof ? cs : g0);
+    const float* q1 = a.q + cell0 * qst + (a.q_per_dof ? cs + 1 : g1);
+    float* o_p = SWEEP ? a.out + fidx(xs, 0, cs, g.ny, a.out_h, g.C)
+                       : (a.r ? a.r + fidx(xs, 0, cs, g.ny, a.r_h, g.C) : nullptr);
+    float* avg_p = EMA && act ? a.avg + fidx(x, 0, cs, g.ny, a.avg_h, g.C) : nullptr;
+    const float2 beta2 = bc2(a.beta);
+    const float2 strm2 = a.strm ? make_float2(a.strm[n0], a.strm[n1]) : bc2(0.f);
+    const int oy0 = max(ya, 0), oy1 = yb;
+    const int lane_off = ty * CC + 2 * tx;          // this lane's pair in a staged row
+
+    float2 rA[T], rB[T], rC[T], rD[T];              // pending outputs, by (y - ya) mod T
+#pragma unroll
+    for (int i = 0; i < T; ++i) rA[i] = rB[i] = rC[i] = rD[i] = bc2(0.f);
+
+    if (producer) {
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (k < nsteps) issue(k, k);
+    }
+    double l1 = 0.0;
+    int slot = 0;          // slot of the current step (k mod S)
+    unsigned fpar = 0;     // parity of the current fill of `slot`
+    float2 sgN = bc2(0.f), qN = bc2(0.f);
+    if (act) {
+        sgN = make_float2(sig0[ya * g.ng], sig1[ya * g.ng]);
+        qN = make_float2(q0[ya * qst], q1[ya * qst]);
+    }
+
+#define TMA_STEP(K, SK, OUT, Y)                                                       \
+    {                                                                                 \
+        const int k_ = (K);                                                           \
+        float2 sg_ = sgN, q_ = qN;                                                    \
+        if ((OUT) && act && (Y) + 1 < yb) {                                           \
+            sgN = make_float2(sig0[((Y) + 1) * g.ng], sig1[((Y) + 1) * g.ng]);       \
+            qN = make_float2(q0[((Y) + 1) * qst], q1[((Y) + 1) * qst]);              \
+        }                                                                             \
+        mbar_wait(&full[slot], fpar);                                                 \
+        const float* buf_ = sm + slot * (NF * FS);                                    \
+        if (EMA && avg_p) {                                                           \
+            const int yl_ = ya - L + k_;                                              \
+            if (yl_ >= oy0 && yl_ < oy1) {                                            \
+                const float2 p_ = ld2(buf_ + L * CC + lane_off);                      \
+                float2 o_ = p_;                                                       \
+                if (a.avg_mode == 2) {                                                \
+                    const float2 b_ = ld2(buf_ + 3 * FS + lane_off);                  \
+                    o_ = make_float2(__fmaf_rn(b_.x, a.omt, __fmul_rn(a.theta, p_.x)),   \
+                                     __fmaf_rn(b_.y, a.omt, __fmul_rn(a.theta, p_.y)));  \
+                }                                                                     \
+                st2(avg_p + (int64_t)yl_ * g.C, o_);                                  \
+            }                                                                         \
+        }                                                                             \
+        float2 a_g = bc2(0.f), a_m = a_g, a_s = a_g, a_sk = a_g, a_k = a_g, a_mk = a_g, a_ky = a_g; \
+        {                                                                             \
+            const float* bp_ = buf_ + lane_off;                                       \
+            _Pragma("unroll") for (int t_ = 0; t_ < T; ++t_) {                        \
+                float2 p_ = ld2(bp_ + t_ * CC);                                       \
+                if (SWEEP) p_ = sub2(p_, ld2(bp_ + 3 * FS + t_ * CC));                \
+                const float2 k1_ = ld2(bp_ + FS + t_ * CC);                          \
+                const float2 k2_ = ld2(bp_ + 2 * FS + t_ * CC);                      \
+                a_g = fma2c((float)TP::g(t_), p_, a_g);                               \
+                a_m = fma2c((float)TP::m(t_), p_, a_m);                               \
+                a_s = fma2c((float)TP::s(t_), p_, a_s);                               \
+                a_sk = fma2c((float)TP::s(t_), mul2(p_, k1_), a_sk);                  \
+                a_k = fma2c((float)TP::s(t_), k1_, a_k);                              \
+                a_mk = fma2c((float)TP::m(t_), mul2(p_, k2_), a_mk);                  \
+                a_ky = fma2c((float)TP::m(t_), k2_, a_ky);                            \
+            }                                                                         \
+        }                                                                             \
+        const float2 xa_ = fma2(mu_dx, a_g, mul2(hx, a_sk));                          \
+        const float2 xg_ = mul2(nu_dy, a_m);                                          \
+        const float2 xs_ = mul2(hy, a_mk);                                            \
+        const float2 xd1_ = mul2(mhx, a_k);                                           \
+        const float2 xd2_ = mul2(mhy, a_ky);                                          \
+        _Pragma("unroll") for (int i_ = 0; i_ < T; ++i_) {                            \
+            const int sl_ = ((SK) + i_) % T;                                          \
+            const int b_ = 2 * L - i_;                                                \
+            const float m_ = (float)TP::m(b_), gt_ = (float)TP::g(b_), s_ = (float)TP::s(b_); \
+            if (i_ == 2 * L) {                                                        \
+                rA[sl_] = fma2c(m_, xa_, fma2c(gt_, xg_, mul2(bc2(s_), xs_)));        \
+                rB[sl_] = mul2(bc2(m_), a_s);                                         \
+                rC[sl_] = mul2(bc2(s_), a_m);                                         \
+                rD[sl_] = fma2c(m_, xd1_, mul2(bc2(s_), xd2_));                       \
+            } else {                                                                  \
+                rA[sl_] = fma2c(m_, xa_, fma2c(gt_, xg_, fma2c(s_, xs_, rA[sl_])));   \
+                rB[sl_] = fma2c(m_, a_s, rB[sl_]);                                    \
+                rC[sl_] = fma2c(s_, a_m, rC[sl_]);                                    \
+                rD[sl_] = fma2c(m_, xd1_, fma2c(s_, xd2_, rD[sl_]));                  \
+            }                                                                         \
+        }                                                                             \
+        const int cs_ = slot >= L ? slot - L : slot - L + S;  /* centre row's slot */ \
+        if ((OUT) && act && (Y) < yb) {                                               \
+            const int y_ = (Y);                                                       \
+            const float* cb_ = sm + cs_ * (NF * FS) + L * CC + lane_off;              \
+            float2 pc_ = ld2(cb_);                                                    \
+            if (SWEEP) pc_ = sub2(pc_, ld2(cb_ + 3 * FS));                            \
+            const float2 kxc_ = ld2(cb_ + FS), kyc_ = ld2(cb_ + 2 * FS);             \
+            float2 r_ = fma2(hx, mul2(kxc_, rB[SK]), rA[SK]);                         \
+            r_ = fma2(hy, mul2(kyc_, rC[SK]), r_);                                    \
+            r_ = sub2(fma2(pc_, add2(rD[SK], sg_), r_), q_);                          \
+            if (SWEEP) {                                                              \
+                const float2 d_ = mul2(beta2, add2(strm2, sg_));                      \
+                const float2 inv_ = make_float2(rcp_nr(d_.x), rcp_nr(d_.y));          \
+                float2 qt_ = mul2(r_, inv_);                                          \
+                if (a.refine_div)                                                     \
+                    qt_ = fma2(fma2(make_float2(-d_.x, -d_.y), qt_, r_), inv_, qt_);  \
+                st2(o_p + (int64_t)y_ * g.C, sub2(pc_, qt_));                         \
+            } else {                                                                  \
+                if (o_p) st2(o_p + (int64_t)y_ * g.C, r_);                           \
+                l1 += fabs((double)r_.x) + fabs((double)r_.y);                        \
+            }                                                                         \
+        }                                                                             \
+        if (k_ >= L) {                       /* last read of the centre row's slot */ \
+            __syncwarp();                                                             \
+            if (tx == 0) mbar_arrive(&empty[cs_]);                                    \
+        }                                                                             \
+        if (producer && k_ + P < nsteps) {                                            \
+            const int is_ = slot + P >= S ? slot + P - S : slot + P;                  \
+            const int fill_ = (k_ + P) / S;                                           \
+            if (fill_ >= 1) mbar_wait(&empty[is_], (unsigned)((fill_ - 1) & 1));      \
+            issue(k_ + P, is_);                                                       \
+        }                                                                             \
+        if (++slot == S) { slot = 0; fpar ^= 1u; }                                    \
+    }
+
+    // prologue: lead rows ya-L .. ya+L-1 (outputs below ya are never emitted)
+#pragma unroll
+    for (int k = 0; k < 2 * L; ++k) TMA_STEP(k, (k + 1) % T, false, 0);
+
+    int kbase = 2 * L;
+    for (int y0 = ya; y0 < yb; y0 += T, kbase += T) {
+#pragma unroll
+        for (int s = 0; s < T; ++s) TMA_STEP(kbase + s, s, true, y0 + s);
+    }
+#undef TMA_STEP
+    if (!SWEEP && a.partials) {
+        const double tot = block_sum(l1, red);
+        if (threadIdx.x == 0 && threadIdx.y == 0)
+            a.partials[((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = tot;
+    }
+}
+
+}  // namespace csn

@@ -156,8 +156,9 @@ pg_residual_x2_kernel(const PGResidArgs<float> a) {
                         const float* p_ = buf_ + (e / G4) * CC + (e % G4) * VEC;      \
                         float* o_ = avg_p[i] + (int64_t)yl_ * g.C;                    \
                         _Pragma("unroll") for (int v = 0; v < VEC; ++v)               \
-                            o_[v] = a.avg_mode == 2 ? p_[3 * FS + v] * a.omt + a.theta * p_[v] \
-                                                    : p_[v];                          \
+                            o_[v] = a.avg_mode == 2                                   \
+                                        ? __fmaf_rn(p_[3 * FS + v], a.omt, __fmul_rn(a.theta, p_[v])) \
+                                        : p_[v];                                      \
                     }                                                                 \
                 }                                                                     \
             }                                                                         \
@@ -360,7 +361,7 @@ pg_diffusivity_x2_kernel(const PGKArgs<float> a) {
 #pragma unroll
                         for (int vv = 0; vv < VEC; ++vv) {
                             pv[vv] = p[vv];
-                            if (EMA) pv[vv] = p[FS + vv] * omt + theta * pv[vv];
+                            if (EMA) pv[vv] = __fmaf_rn(p[FS + vv], omt, __fmul_rn(theta, pv[vv]));
                             p[vv] = pv[vv];
                         }
                         if (own_ptr[i] && own_row) {
@@ -528,7 +529,7 @@ pg_grad_x2_kernel(const PGKArgs<float> a, float* __restrict__ gx_out,
         cp_async_commit();
     }
     // K: step (lead row ya - L + K); KR = K mod T (compile time); output row Y = lead - l
-#define K2A_STEP(K, KR, OUT, Y)                                                           {                                                                                         const int k_ = (K);                                                                   const int yl_ = ya - L + k_;                                                          cp_async_wait<S - 2>();                                                               float* buf_ = sm + (size_t)(k_ % S) * NF * FS;                                        if (EMA || write_avg) {                                                                   const bool own_row_ = yl_ >= oy0 && yl_ < oy1;                                       _Pragma("unroll") for (int i = 0; i < NI; ++i) {                                          const int e = tid + i * NT;                                                           if (e < W * G4) {                                                                         float* p_ = buf_ + (e / G4) * CC + (e % G4) * VEC;                                    float pv_[VEC];                                                                       _Pragma("unroll") for (int vv = 0; vv < VEC; ++vv) {                                      pv_[vv] = p_[vv];                                                                     if (EMA) pv_[vv] = p_[FS + vv] * omt + theta * pv_[vv];                               p_[vv] = pv_[vv];                                                                 }                                                                                     if (own_ptr[i] && own_row_) {                                                             float* o_ = own_ptr[i] + (int64_t)yl_ * g.C;                                          _Pragma("unroll") for (int vv = 0; vv < VEC; ++vv) o_[vv] = pv_[vv];                     }                                                                                 }                                                                                 }                                                                                 }                                                                                     __syncthreads();                                                                      {                                                                                         float2 ag_ = bc2(0.f), am_ = ag_;                                                     const float* bp_ = buf_ + lane;                                                       _Pragma("unroll") for (int t = 0; t < T; ++t) {                                           const float2 p_ = ld2(bp_ + t * CC);                                                  ag_ = fma2c((float)TP::g(t), p_, ag_);                                                am_ = fma2c((float)TP::m(t), p_, am_);                                            }                                                                                     rG[(KR)] = ag_;                                                                       rM[(KR)] = am_;                                                                   }                                                                                     if ((OUT) && act && (Y) < yb) {                                                           float2 px_ = bc2(0.f), py_ = px_;                                                     _Pragma("unroll") for (int b = 0; b < T; ++b) {                                           px_ = fma2c((float)TP::m(b), rG[((KR) + 1 + b) % T], px_);                            py_ = fma2c((float)TP::g(b), rM[((KR) + 1 + b) % T], py_);                        }                                                                                     const int64_t o_ = ob + (int64_t)(Y) * g.C;                                           st2(gx_out + o_, mul2(px_, inv_dx));                                                  st2(gy_out + o_, mul2(py_, inv_dy));                                              }                                                                                     if (k_ + S - 1 < nsteps)                                                                  st.issue(ya - L + k_ + S - 1, sbase + ((k_ + S - 1) % S) * NF * FSB, FSB, a.psi);         cp_async_commit();                                                                }
+#define K2A_STEP(K, KR, OUT, Y)                                                           {                                                                                         const int k_ = (K);                                                                   const int yl_ = ya - L + k_;                                                          cp_async_wait<S - 2>();                                                               float* buf_ = sm + (size_t)(k_ % S) * NF * FS;                                        if (EMA || write_avg) {                                                                   const bool own_row_ = yl_ >= oy0 && yl_ < oy1;                                       _Pragma("unroll") for (int i = 0; i < NI; ++i) {                                          const int e = tid + i * NT;                                                           if (e < W * G4) {                                                                         float* p_ = buf_ + (e / G4) * CC + (e % G4) * VEC;                                    float pv_[VEC];                                                                       _Pragma("unroll") for (int vv = 0; vv < VEC; ++vv) {                                      pv_[vv] = p_[vv];                                                                     if (EMA) pv_[vv] = __fmaf_rn(p_[FS + vv], omt, __fmul_rn(theta, pv_[vv]));                               p_[vv] = pv_[vv];                                                                 }                                                                                     if (own_ptr[i] && own_row_) {                                                             float* o_ = own_ptr[i] + (int64_t)yl_ * g.C;                                          _Pragma("unroll") for (int vv = 0; vv < VEC; ++vv) o_[vv] = pv_[vv];                     }                                                                                 }                                                                                 }                                                                                 }                                                                                     __syncthreads();                                                                      {                                                                                         float2 ag_ = bc2(0.f), am_ = ag_;                                                     const float* bp_ = buf_ + lane;                                                       _Pragma("unroll") for (int t = 0; t < T; ++t) {                                           const float2 p_ = ld2(bp_ + t * CC);                                                  ag_ = fma2c((float)TP::g(t), p_, ag_);                                                am_ = fma2c((float)TP::m(t), p_, am_);                                            }                                                                                     rG[(KR)] = ag_;                                                                       rM[(KR)] = am_;                                                                   }                                                                                     if ((OUT) && act && (Y) < yb) {                                                           float2 px_ = bc2(0.f), py_ = px_;                                                     _Pragma("unroll") for (int b = 0; b < T; ++b) {                                           px_ = fma2c((float)TP::m(b), rG[((KR) + 1 + b) % T], px_);                            py_ = fma2c((float)TP::g(b), rM[((KR) + 1 + b) % T], py_);                        }                                                                                     const int64_t o_ = ob + (int64_t)(Y) * g.C;                                           st2(gx_out + o_, mul2(px_, inv_dx));                                                  st2(gy_out + o_, mul2(py_, inv_dy));                                              }                                                                                     if (k_ + S - 1 < nsteps)                                                                  st.issue(ya - L + k_ + S - 1, sbase + ((k_ + S - 1) % S) * NF * FSB, FSB, a.psi);         cp_async_commit();                                                                }
 #pragma unroll
     for (int k = 0; k < 2 * L; ++k) K2A_STEP(k, k % T, false, 0);
     int kb = 2 * L;

@@ -212,6 +212,7 @@ class DDCycleEngine(CycleEngine):
         self.lg = lg
         self.x0_levels = x0_levels
         super().__init__(local_h, n_group, dtype, device)
+        self.pad_delta = False         # x-ghosted finest correction (see correction)
         west, east = comm.rank > 0, comm.rank < comm.size - 1
         self.geoms = [lev.geom(n_group, int(west), int(east)) for lev in local_h.levels]
         self.sigma = sigma_ghosted
@@ -237,7 +238,7 @@ class DDCycleEngine(CycleEngine):
     def _hook_l1(self):
         self.comm.allreduce_sum_(self.l1)
 
-    def correction(self, r0, n_sweeps, finest_scale):
+    def correction(self, r0, n_sweeps, finest_scale, out0=None, out0_halo=0):
         if n_sweeps > UP_MAX_SWEEPS:
             raise ValueError("domain decomposition supports <= 3 Jacobi sweeps per level")
         L = self.h.levels

@@ -197,7 +197,7 @@ def _run_cycles(psi, setup, n_iters, fission_frozen=None, pg_state=None, scheme=
             scalar_flux_into(psi, setup.quad, bufs.phi)
             assemble_group_source(bufs.phi, setup.mat, 0.0, d.dtype, bufs.q, fission_frozen)
         res = eng.cycle(psi, bufs.q, setup.filters, opts.pg, scheme, opts.jacobi_sweeps,
-                        opts.pg_sweeps, pg_state)
+                        opts.pg_sweeps, pg_state, halo_ok=bool(history))
         history.append(res)
         if not math.isfinite(res):
             break
@@ -317,9 +317,11 @@ class Solver:
                 self._fis = self._frozen_fission(1.0 if boot else 1.0 / self.k)
             fission = self._fis
         q = self._source(fission, self.in_phase == 0)
+        # psi's halo is consistent: zero start / applied boundary at setup, then every
+        # cycle ends with the boundary (uniform rescaling keeps it)
         res = self.eng.cycle(self.psi, q, self.setup.filters, opts.pg,
                              "upwind" if boot else opts.scheme, opts.jacobi_sweeps,
-                             opts.pg_sweeps, None if boot else self.pgs)
+                             opts.pg_sweeps, None if boot else self.pgs, halo_ok=True)
         (self.boot_history if boot else self.history).append(res)
         self.in_phase += 1
         finite = math.isfinite(res)

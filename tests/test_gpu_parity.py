@@ -403,3 +403,60 @@ def test_upwind_x2_matches_scalar(P, nx, ny, na, ng, scale):
     torch.cuda.synchronize()
     assert torch.equal(out[1], out[0])
     assert torch.equal(out[(1, "sweep")], out[(0, "sweep")])
+
+
+@pytest.mark.parametrize("nx,ny,na,ng,p", [(32, 24, 8, 1, 3), (20, 18, 4, 2, 2), (16, 13, 2, 1, 1),
+                                           (24, 20, 2, 3, 5), (40, 32, 16, 1, 3)])
+def test_tma_residual_matches_cp_async(P, nx, ny, na, ng, p):
+    """The TMA/mbarrier residual kernels (K3, K3+EMA, fused sweep K5) write the same
+    r, iterate average, L1 and swept psi, bit for bit, as the cp.async kernels, when
+    the staged halos are consistent (boundary applied, k zero outside its band)."""
+    from paper_2301_09991_b200 import _lib
+    from paper_2301_09991_b200.discretisation import pg_residual_launch
+    rng = np.random.default_rng(5)
+    q = P.build_quadrature(na)
+    dx, dy = 1.0 / nx, 1.3 / ny
+    h, l = 3 * p, p
+    grid = P.GridSpec(nx, ny, dx, dy, h)
+    fs = P.build_convfem_filters(p, dx, dy)
+    shp = (nx + 2 * h, ny + 2 * h, q.n_dir, ng)
+    psi = P.Field(grid, q.n_dir, ng, rng.standard_normal(shp), dtype=F32)
+    P.apply_boundary(psi, q)
+    kband = np.zeros(shp)
+    kband[h - l:h + nx + l, h - l:h + ny + l] = rng.uniform(0, 0.02, (nx + 2 * l, ny + 2 * l,
+                                                                      q.n_dir, ng))
+    kx = torch.as_tensor(kband, dtype=F32, device="cuda")
+    ky = torch.as_tensor(kband[::-1, ::-1].copy(), dtype=F32, device="cuda")
+    ky[:h - l] = 0; ky[h + nx + l:] = 0; ky[:, :h - l] = 0; ky[:, h + ny + l:] = 0
+    delta = P.Field(grid, q.n_dir, ng, 0.1 * rng.standard_normal(shp), dtype=F32)
+    P.apply_boundary(delta, q)
+    sig = torch.as_tensor(rng.uniform(0.2, 4.0, (nx, ny, ng)), dtype=F32, device="cuda")
+    qt = torch.as_tensor(rng.standard_normal((nx, ny, q.n_dir, ng)), dtype=F32, device="cuda")
+    avg0 = torch.as_tensor(rng.standard_normal(shp), dtype=F32, device="cuda")
+    qd = q.device(F32, torch.device("cuda"), dx, dy)
+    npart = _lib.load().csn_partials_size(_lib.F32, _lib.geom(nx, ny, q.n_dir, ng, na, dx, dy), p)
+    out = {}
+    for v in (1, 0):
+        prev = _lib.set_tuning("pg_tma", v)
+        try:
+            res = []
+            for ema in (0, 1, 2):
+                r = torch.zeros((nx, ny, q.n_dir, ng), dtype=F32, device="cuda")
+                a = avg0.clone()
+                parts = torch.zeros(int(npart), dtype=torch.float64, device="cuda")
+                l1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+                pg_residual_launch(psi, None, None, q, fs, kx, ky, h, r=r, r_halo=0,
+                                   partials=parts, l1=l1, sigma=sig, qt=qt, per_dof=1, consts=qd,
+                                   avg=a if ema else None, avg_mode=ema, theta=0.2)
+                res += [r, a, l1]
+            sw = torch.zeros_like(psi.data)
+            pg_residual_launch(psi, None, None, q, fs, kx, ky, h, psi_out=sw, out_halo=h,
+                               delta=delta.data, delta_halo=h, beta=3.0, sigma=sig, qt=qt,
+                               per_dof=1, consts=qd)
+            res.append(sw)
+            torch.cuda.synchronize()
+            out[v] = [t.clone() for t in res]
+        finally:
+            _lib.set_tuning("pg_tma", prev)
+    for i, (t1, t0) in enumerate(zip(out[1], out[0])):
+        assert torch.equal(t1, t0), i
