@@ -24,6 +24,7 @@ int g_tune_upwind_x2 = 1;
 int g_tune_upwind_div = 3;
 int g_tune_sweep_div = 1;
 int g_tune_pg_tma = 1;
+int g_tune_upwind_tma = 0;
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -40,6 +41,20 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
             cudaGetLastError();
     }
     return fn;
+}
+
+// tiled fp32 map of rank 2 or 3 (dims / box innermost first, strides in bytes)
+bool raw_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
+             const cuuint64_t* strides, const cuuint32_t* box) {
+    auto enc = tensor_map_encoder();
+    if (!enc || !base || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+    for (int i = 0; i + 1 < rank; ++i)
+        if (strides[i] % 16) return false;
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), dims, strides,
+               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
 }
 
 // 3D map over a padded fp32 field [nx + 2h][ny + 2h][C]: box = 64 channels x 1 row x bx
@@ -347,6 +362,39 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
             a.xchunk = (int)cdiv(g->nx, chunks);
             const int gz = (int)cdiv(g->nx, a.xchunk);
             dim3 grid(gx, gy, gz), block(32, UPX_SPB);
+            // TMA-staged columns (upwind_smooth_tma_kernel) where its layout applies
+            // (default off: measured on C4 1.18 ms vs 1.15 ms for the register kernel —
+            // both sit at ~47% of DRAM bandwidth with 16 warps/SM, so the deeper
+            // prefetch does not pay for its shared-memory reads)
+            if (g_tune_upwind_tma && g1 && a.exact_div == 3 && init_mode != 1 && g->na >= 8 &&
+                g->na <= 32 && g->ny % 4 == 0 && !g->ghost_w && !g->ghost_e &&
+                (init_mode == 0 || (init_h == 0 && a.angle_coarsens))) {
+                UpTmaMaps maps;
+                const cuuint64_t C64 = (cuuint64_t)C;
+                cuuint64_t sd[3] = {C64, (cuuint64_t)g->ny, (cuuint64_t)g->nx};
+                cuuint64_t ss[2] = {C64 * 4, C64 * 4 * g->ny};
+                cuuint32_t sb[3] = {UPX_CC, UPT_ROWS, 1};
+                cuuint64_t gd[2] = {(cuuint64_t)g->ny, (cuuint64_t)g->nx};
+                cuuint64_t gs[1] = {(cuuint64_t)g->ny * 4};
+                cuuint32_t gb[2] = {UPT_SIGROWS, 1};
+                bool ok = raw_map(&maps.src, src, 3, sd, ss, sb) &&
+                          raw_map(&maps.sigma, sigma, 2, gd, gs, gb);
+                if (ok && init_mode == 2) {
+                    const cuuint64_t Cc = (cuuint64_t)gc->nd * gc->ng;
+                    cuuint64_t id[3] = {Cc, (cuuint64_t)gc->ny, (cuuint64_t)gc->nx};
+                    cuuint64_t is[2] = {Cc * 4, Cc * 4 * gc->ny};
+                    cuuint32_t ib[3] = {UPT_CCH, UPT_CROWS, 1};
+                    ok = raw_map(&maps.init, init, 3, id, is, ib);
+                } else if (ok) {
+                    maps.init = maps.src;   // unused (mode 0)
+                }
+                if (ok) {
+                    upwind_smooth_tma_kernel<<<grid, block, 0, st>>>(a, maps);
+                    CSN_CHECK_LAUNCH();
+                    return CSN_OK;
+                }
+                cudaGetLastError();
+            }
             auto go = [&](auto g1t, auto dmt) {
                 upwind_smooth_x2_kernel<3, decltype(g1t)::value, decltype(dmt)::value>
                     <<<grid, block, 0, st>>>(a);
@@ -409,6 +457,7 @@ int csn_set_tuning(const char* key, int value, int* prev) {
     if (!strcmp(key, "upwind_div")) slot = &g_tune_upwind_div;
     if (!strcmp(key, "sweep_div")) slot = &g_tune_sweep_div;
     if (!strcmp(key, "pg_tma")) slot = &g_tune_pg_tma;
+    if (!strcmp(key, "upwind_tma")) slot = &g_tune_upwind_tma;
     if (!slot) return CSN_E_ARG;
     if (prev) *prev = *slot;
     *slot = value;

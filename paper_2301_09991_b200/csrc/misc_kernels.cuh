@@ -150,23 +150,37 @@ boundary_kernel(Geo g, Real* f, int h, const Real* mu, const Real* nu) {
     const int n_cells = n_rowcells + g.nx * 2 * h;
     const int n = c / g.ng;
     const bool mpos = mu[n] > Real(0), npos = nu[n] > Real(0);
-    for (int k = blockIdx.y; k < n_cells; k += gridDim.y) {
-        int xs, ys;   // storage coordinates
-        if (k < n_rowcells) {
-            const int r = k / NY;
-            ys = k - r * NY;
-            xs = r < h ? r : g.nx + r;
-        } else {
-            const int kk = k - n_rowcells;
-            const int r = kk / (2 * h);
-            const int cidx = kk - r * 2 * h;
-            xs = h + r;
-            ys = cidx < h ? cidx : g.ny + cidx;
+    // BC cells per trip: all loads in flight before the stores (latency, not bandwidth,
+    // bounds a one-cell-per-trip loop)
+    constexpr int BC = 4;
+    for (int k0 = blockIdx.y; k0 < n_cells; k0 += BC * gridDim.y) {
+        int64_t dst[BC];
+        Real v[BC];
+#pragma unroll
+        for (int u = 0; u < BC; ++u) {
+            const int k = k0 + u * gridDim.y;
+            dst[u] = -1;
+            v[u] = Real(0);
+            if (k >= n_cells) continue;
+            int xs, ys;   // storage coordinates
+            if (k < n_rowcells) {
+                const int r = k / NY;
+                ys = k - r * NY;
+                xs = r < h ? r : g.nx + r;
+            } else {
+                const int kk = k - n_rowcells;
+                const int r = kk / (2 * h);
+                const int cidx = kk - r * 2 * h;
+                xs = h + r;
+                ys = cidx < h ? cidx : g.ny + cidx;
+            }
+            int x = xs - h, y = ys - h;
+            if (resolve_vac(x, y, g, mpos, npos)) v[u] = f[fidx(x, y, c, g.ny, h, g.C)];
+            dst[u] = ((int64_t)xs * NY + ys) * g.C + c;
         }
-        int x = xs - h, y = ys - h;
-        Real v = Real(0);
-        if (resolve_vac(x, y, g, mpos, npos)) v = f[fidx(x, y, c, g.ny, h, g.C)];
-        f[((int64_t)xs * NY + ys) * g.C + c] = v;
+#pragma unroll
+        for (int u = 0; u < BC; ++u)
+            if (dst[u] >= 0) f[dst[u]] = v[u];
     }
 }
 

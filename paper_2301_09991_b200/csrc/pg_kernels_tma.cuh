@@ -19,9 +19,8 @@
 // with its boundary applied); the frozen-cycle iterate average reads pbar_old through
 // a second (8-cell) box and writes pbar from the consuming thread.
 #pragma once
-#include <cuda.h>
-
 #include "pg_kernels_x2.cuh"
+#include "tma_util.cuh"
 
 namespace csn {
 
@@ -29,45 +28,21 @@ struct PGTmaMaps {
     CUtensorMap psi, kx, ky, aux;   // aux: delta (sweep) or pbar_old (EMA)
 };
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "MBW_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra MBW_%=;\n"
-        "}\n" ::"r"(smem_u32(b)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1, int c2) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-        : "memory");
-}
+// ring geometry: a slot holds psi, kx, ky rows (W cells) plus delta (W cells, sweep) or
+// pbar_old (the CTA's PG_TX cells, EMA); PREFETCH rows are in flight ahead of the
+// lead row
+template <int L, int MODE>
+struct TmaRing {
+    static constexpr int FS = (PG_TX + 2 * L) * X2_CC;
+    static constexpr int SLOT = 3 * FS + (MODE == PG_SWEEP ? FS : MODE == PG_RESID_EMA ? PG_TX * X2_CC : 0);
+    static constexpr int PREFETCH = L > 3 ? 2 : 3;   // 4-5 measured slower (C4: spills, less L1)
+    static constexpr int S = L + 1 + PREFETCH;
+};
 
 template <int L, int MODE>
 constexpr size_t pg_residual_tma_smem() {
-    return (size_t)X2Stages<L>::value * (MODE == PG_RESID ? 3 : 4) * (PG_TX + 2 * L) * X2_CC *
-               sizeof(float) + 128;   // + alignment slack (TMA destinations: 128 B)
+    return (size_t)TmaRing<L, MODE>::S * TmaRing<L, MODE>::SLOT * sizeof(float) +
+           128;   // + alignment slack (TMA destinations: 128 B)
 }
 
 template <int L, int MODE>
@@ -80,9 +55,10 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
     constexpr int CC = X2_CC;
     constexpr int W = PG_TX + 2 * L;
     constexpr int NF = MODE == PG_RESID ? 3 : 4;
-    constexpr int S = X2Stages<L>::value;
+    constexpr int S = TmaRing<L, MODE>::S;
     constexpr int P = S - L - 1;
     constexpr int FS = W * CC;                     // floats per field row
+    constexpr int SLOT = TmaRing<L, MODE>::SLOT;
     constexpr unsigned ROWB = W * CC * sizeof(float);
     constexpr unsigned TXB = 3 * ROWB + (SWEEP ? ROWB : 0) + (EMA ? PG_TX * CC * sizeof(float) : 0);
     extern __shared__ unsigned char smraw[];
@@ -123,7 +99,7 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
     // producer: lead row ya - L + k of every field into slot s
     auto issue = [&](int k, int s) {
         const int yy = ya - L + k;
-        float* dst = sm + s * (NF * FS);
+        float* dst = sm + s * SLOT;
         mbar_expect_tx(&full[s], TXB);
         tma_load_3d(dst, &m.psi, &full[s], c0, yy + a.psi_h, x0 - L + a.psi_h);
         tma_load_3d(dst + FS, &m.kx, &full[s], c0, yy + a.k_h, x0 - L + a.k_h);
@@ -175,7 +151,7 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
             qN = make_float2(q0[((Y) + 1) * qst], q1[((Y) + 1) * qst]);              \
         }                                                                             \
         mbar_wait(&full[slot], fpar);                                                 \
-        const float* buf_ = sm + slot * (NF * FS);                                    \
+        const float* buf_ = sm + slot * SLOT;                                         \
         if (EMA && avg_p) {                                                           \
             const int yl_ = ya - L + k_;                                              \
             if (yl_ >= oy0 && yl_ < oy1) {                                            \
@@ -230,7 +206,7 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
         const int cs_ = slot >= L ? slot - L : slot - L + S;  /* centre row's slot */ \
         if ((OUT) && act && (Y) < yb) {                                               \
             const int y_ = (Y);                                                       \
-            const float* cb_ = sm + cs_ * (NF * FS) + L * CC + lane_off;              \
+            const float* cb_ = sm + cs_ * SLOT + L * CC + lane_off;                    \
             float2 pc_ = ld2(cb_);                                                    \
             if (SWEEP) pc_ = sub2(pc_, ld2(cb_ + 3 * FS));                            \
             const float2 kxc_ = ld2(cb_ + FS), kyc_ = ld2(cb_ + 2 * FS);             \

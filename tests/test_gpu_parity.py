@@ -376,7 +376,8 @@ def test_checkpoint_resume_bitwise(P, tmp_path, tag, dtype, split):
 
 
 @pytest.mark.parametrize("nx,ny,na,ng,scale", [(48, 40, 8, 1, 3.0), (32, 38, 8, 2, 1.0),
-                                               (40, 24, 4, 4, 3.0), (64, 64, 16, 1, 3.0)])
+                                               (40, 24, 4, 4, 3.0), (64, 64, 16, 1, 3.0),
+                                               (36, 44, 32, 1, 1.0), (16, 68, 8, 1, 3.0)])
 def test_upwind_x2_matches_scalar(P, nx, ny, na, ng, scale):
     """The packed channel-pair smoother (fp32) is bit-identical to the scalar kernel on
     every level it takes (face channel count a multiple of 64), incl. ragged strips."""
@@ -389,8 +390,9 @@ def test_upwind_x2_matches_scalar(P, nx, ny, na, ng, scale):
     r = torch.as_tensor(rng.standard_normal((nx, ny, q.n_dir, ng)), dtype=F32, device="cuda")
     qfull = rng.standard_normal((nx, ny, q.n_dir, ng))
     out = {}
-    for v in (1, 0):
-        prev = _lib.set_tuning("upwind_x2", v)
+    for v in (2, 1, 0):     # 2: packed + TMA-staged columns, 1: packed, 0: scalar
+        prev = _lib.set_tuning("upwind_x2", min(v, 1))
+        prev_t = _lib.set_tuning("upwind_tma", 1 if v == 2 else 0)
         try:
             eng = hier.engine(ng, F32, r.device)
             out[v] = eng.correction(r, 3, scale).clone()
@@ -400,7 +402,9 @@ def test_upwind_x2_matches_scalar(P, nx, ny, na, ng, scale):
             out[(v, "sweep")] = sw.data.clone()
         finally:
             _lib.set_tuning("upwind_x2", prev)
+            _lib.set_tuning("upwind_tma", prev_t)
     torch.cuda.synchronize()
+    assert torch.equal(out[2], out[0])
     assert torch.equal(out[1], out[0])
     assert torch.equal(out[(1, "sweep")], out[(0, "sweep")])
 
