@@ -464,3 +464,40 @@ def test_tma_residual_matches_cp_async(P, nx, ny, na, ng, p):
             _lib.set_tuning("pg_tma", prev)
     for i, (t1, t0) in enumerate(zip(out[1], out[0])):
         assert torch.equal(t1, t0), i
+
+
+@pytest.mark.parametrize("nx,ny,na,ng,p", [(32, 24, 8, 1, 3), (20, 18, 4, 2, 2), (16, 13, 2, 1, 1),
+                                           (40, 32, 16, 1, 3)])
+def test_split_diffusivities_match_fused(P, nx, ny, na, ng, p):
+    """K2 through the workspace (K2a gradients + K2b packed k formula) gives the same k and
+    iterate average, bit for bit, as the fused two-stage kernel (scalar k formula)."""
+    from paper_2301_09991_b200.discretisation import diffusivities_into, diffusivities_workspace
+    rng = np.random.default_rng(9)
+    q = P.build_quadrature(na)
+    dx, dy = 1.0 / nx, 1.3 / ny
+    h = 3 * p
+    grid = P.GridSpec(nx, ny, dx, dy, h)
+    fs = P.build_convfem_filters(p, dx, dy)
+    cfg = P.PGConfig()
+    shp = (nx + 2 * h, ny + 2 * h, q.n_dir, ng)
+    psi = torch.as_tensor(rng.standard_normal(shp), dtype=F32, device="cuda")
+    avg0 = torch.as_tensor(rng.standard_normal(shp), dtype=F32, device="cuda")
+    qd = q.device(F32, torch.device("cuda"), dx, dy)
+    from paper_2301_09991_b200 import _lib
+    gm = _lib.geom(nx, ny, q.n_dir, ng, na, dx, dy)
+    work = diffusivities_workspace(psi, gm, p)
+    assert work is not None
+    for mode in (0, 1, 2):
+        out = []
+        for w in (None, work):
+            kx, ky = torch.zeros_like(psi), torch.zeros_like(psi)
+            a_in = avg0.clone() if mode == 2 else None
+            a_out = torch.zeros_like(psi) if mode else None
+            diffusivities_into(psi, grid, q.n_dir, ng, na, fs, cfg, qd["mu"], qd["nu"], kx, ky, h,
+                               avg_in=a_in, avg_out=a_out, avg_mode=mode, theta=0.2, gm=gm,
+                               work=w)
+            torch.cuda.synchronize()
+            out.append((kx, ky, a_out))
+        assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1]), mode
+        if mode:
+            assert torch.equal(out[0][2], out[1][2]), mode
