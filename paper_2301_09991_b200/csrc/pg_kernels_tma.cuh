@@ -61,8 +61,10 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
     constexpr int SLOT = TmaRing<L, MODE>::SLOT;
     constexpr unsigned ROWB = W * CC * sizeof(float);
     constexpr unsigned TXB = 3 * ROWB + (SWEEP ? ROWB : 0) + (EMA ? PG_TX * CC * sizeof(float) : 0);
-    extern __shared__ unsigned char smraw[];
-    float* sm = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+    extern __shared__ __align__(128) unsigned char smraw[];
+    // 128-byte aligned ring base; pointer arithmetic on smraw keeps the shared address
+    // space (a uintptr_t round trip would turn every ring read into a generic LD)
+    float* sm = reinterpret_cast<float*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
     __shared__ double red[32];
     __shared__ __align__(8) uint64_t full[S], empty[S];
 
