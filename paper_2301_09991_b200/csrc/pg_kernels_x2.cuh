@@ -529,7 +529,56 @@ pg_grad_x2_kernel(const PGKArgs<float> a, float* __restrict__ gx_out,
         cp_async_commit();
     }
     // K: step (lead row ya - L + K); KR = K mod T (compile time); output row Y = lead - l
-#define K2A_STEP(K, KR, OUT, Y)                                                           {                                                                                         const int k_ = (K);                                                                   const int yl_ = ya - L + k_;                                                          cp_async_wait<S - 2>();                                                               float* buf_ = sm + (size_t)(k_ % S) * NF * FS;                                        if (EMA || write_avg) {                                                                   const bool own_row_ = yl_ >= oy0 && yl_ < oy1;                                       _Pragma("unroll") for (int i = 0; i < NI; ++i) {                                          const int e = tid + i * NT;                                                           if (e < W * G4) {                                                                         float* p_ = buf_ + (e / G4) * CC + (e % G4) * VEC;                                    float pv_[VEC];                                                                       _Pragma("unroll") for (int vv = 0; vv < VEC; ++vv) {                                      pv_[vv] = p_[vv];                                                                     if (EMA) pv_[vv] = __fmaf_rn(p_[FS + vv], omt, __fmul_rn(theta, pv_[vv]));                               p_[vv] = pv_[vv];                                                                 }                                                                                     if (own_ptr[i] && own_row_) {                                                             float* o_ = own_ptr[i] + (int64_t)yl_ * g.C;                                          _Pragma("unroll") for (int vv = 0; vv < VEC; ++vv) o_[vv] = pv_[vv];                     }                                                                                 }                                                                                 }                                                                                 }                                                                                     __syncthreads();                                                                      {                                                                                         float2 ag_ = bc2(0.f), am_ = ag_;                                                     const float* bp_ = buf_ + lane;                                                       _Pragma("unroll") for (int t = 0; t < T; ++t) {                                           const float2 p_ = ld2(bp_ + t * CC);                                                  ag_ = fma2c((float)TP::g(t), p_, ag_);                                                am_ = fma2c((float)TP::m(t), p_, am_);                                            }                                                                                     rG[(KR)] = ag_;                                                                       rM[(KR)] = am_;                                                                   }                                                                                     if ((OUT) && act && (Y) < yb) {                                                           float2 px_ = bc2(0.f), py_ = px_;                                                     _Pragma("unroll") for (int b = 0; b < T; ++b) {                                           px_ = fma2c((float)TP::m(b), rG[((KR) + 1 + b) % T], px_);                            py_ = fma2c((float)TP::g(b), rM[((KR) + 1 + b) % T], py_);                        }                                                                                     const int64_t o_ = ob + (int64_t)(Y) * g.C;                                           st2(gx_out + o_, mul2(px_, inv_dx));                                                  st2(gy_out + o_, mul2(py_, inv_dy));                                              }                                                                                     if (k_ + S - 1 < nsteps)                                                                  st.issue(ya - L + k_ + S - 1, sbase + ((k_ + S - 1) % S) * NF * FSB, FSB, a.psi);         cp_async_commit();                                                                }
+#define K2A_STEP(K, KR, OUT, Y)                                                                    \
+{                                                                                                  \
+    const int k_ = (K);                                                                            \
+    const int yl_ = ya - L + k_;                                                                   \
+    cp_async_wait<S - 2>();                                                                        \
+    float* buf_ = sm + (size_t)(k_ % S) * NF * FS;                                                 \
+    if (EMA || write_avg) {                                                                        \
+        const bool own_row_ = yl_ >= oy0 && yl_ < oy1;                                             \
+        _Pragma("unroll") for (int i = 0; i < NI; ++i) {                                           \
+            const int e = tid + i * NT;                                                            \
+            if (e < W * G4) {                                                                      \
+                float* p_ = buf_ + (e / G4) * CC + (e % G4) * VEC;                                 \
+                float pv_[VEC];                                                                    \
+                _Pragma("unroll") for (int vv = 0; vv < VEC; ++vv) {                               \
+                    pv_[vv] = p_[vv];                                                              \
+                    if (EMA) pv_[vv] = __fmaf_rn(p_[FS + vv], omt, __fmul_rn(theta, pv_[vv]));     \
+                    p_[vv] = pv_[vv];                                                              \
+                }                                                                                  \
+                if (own_ptr[i] && own_row_) {                                                      \
+                    float* o_ = own_ptr[i] + (int64_t)yl_ * g.C;                                   \
+                    _Pragma("unroll") for (int vv = 0; vv < VEC; ++vv) o_[vv] = pv_[vv];           \
+                }                                                                                  \
+            }                                                                                      \
+        }                                                                                          \
+    }                                                                                              \
+    __syncthreads();                                                                               \
+    {                                                                                              \
+        float2 ag_ = bc2(0.f), am_ = ag_;                                                          \
+        const float* bp_ = buf_ + lane;                                                            \
+        _Pragma("unroll") for (int t = 0; t < T; ++t) {                                            \
+            const float2 p_ = ld2(bp_ + t * CC);                                                   \
+            ag_ = fma2c((float)TP::g(t), p_, ag_);                                                 \
+            am_ = fma2c((float)TP::m(t), p_, am_);                                                 \
+        }                                                                                          \
+        rG[(KR)] = ag_;                                                                            \
+        rM[(KR)] = am_;                                                                            \
+    }                                                                                              \
+    if ((OUT) && act && (Y) < yb) {                                                                \
+        float2 px_ = bc2(0.f), py_ = px_;                                                          \
+        _Pragma("unroll") for (int b = 0; b < T; ++b) {                                            \
+            px_ = fma2c((float)TP::m(b), rG[((KR) + 1 + b) % T], px_);                             \
+            py_ = fma2c((float)TP::g(b), rM[((KR) + 1 + b) % T], py_);                             \
+        }                                                                                          \
+        const int64_t o_ = ob + (int64_t)(Y) * g.C;                                                \
+        st2(gx_out + o_, mul2(px_, inv_dx));                                                       \
+        st2(gy_out + o_, mul2(py_, inv_dy));                                                       \
+    }                                                                                              \
+    if (k_ + S - 1 < nsteps) st.issue(ya - L + k_ + S - 1, sbase + ((k_ + S - 1) % S) * NF * FSB, FSB, a.psi); \
+    cp_async_commit();                                                                             \
+}
 #pragma unroll
     for (int k = 0; k < 2 * L; ++k) K2A_STEP(k, k % T, false, 0);
     int kb = 2 * L;
@@ -596,7 +645,54 @@ pg_kcoef_x2_kernel(const PGKArgs<float> a, const float* __restrict__ gx_in,
         cp_async_commit();
     }
     int slot = 0;
-#define K2B_STEP(K, KR, OUT, Y)                                                           {                                                                                         const int k_ = (K);                                                                   cp_async_wait<P - 1>();                                                               __syncthreads();                                                                      const float* buf_ = sm + slot * (NF * FS) + lane;                                     float2 mx_ = bc2(0.f), my_ = mx_;                                                     _Pragma("unroll") for (int t = 0; t < T; ++t) {                                           mx_ = fma2c((float)TP::m(t), ld2(buf_ + t * CC), mx_);                                my_ = fma2c((float)TP::m(t), ld2(buf_ + FS + t * CC), my_);                       }                                                                                     r2x[(KR)] = mx_;                                                                      r2y[(KR)] = my_;                                                                      if ((OUT) && act && (Y) < yb) {                                                           float2 mmx = bc2(0.f), mmy = mmx;                                                     _Pragma("unroll") for (int b = 0; b < T; ++b) {                                           mmx = fma2c((float)TP::m(b), r2x[((KR) + 1 + b) % T], mmx);                           mmy = fma2c((float)TP::m(b), r2y[((KR) + 1 + b) % T], mmy);                       }                                                                                     const int cs_ = slot >= L ? slot - L : slot - L + S;                                  const float* cb = sm + cs_ * (NF * FS) + L * CC + lane;                               const float2 pxc = ld2(cb), pyc = ld2(cb + FS);                                       const float2 rx = mul2(make_float2(a.alpha_r * mu0, a.alpha_r * mu1), sub2(mmx, pxc));             const float2 ry = mul2(make_float2(a.alpha_r * nu0, a.alpha_r * nu1), sub2(mmy, pyc));             const float amu[2] = {fabsf(mu0), fabsf(mu1)}, anu[2] = {fabsf(nu0), fabsf(nu1)};             const float pxv[2] = {pxc.x, pxc.y}, pyv[2] = {pyc.x, pyc.y};                         const float rxv[2] = {rx.x, rx.y}, ryv[2] = {ry.x, ry.y};                             float kx[2], ky[2];                                                                   _Pragma("unroll") for (int h = 0; h < 2; ++h) {                                           const float bx = fast_div(a.a_abs * a.dx * fabsf(rxv[h]), a.eps + fabsf(pxv[h]));                 const float sx = fast_div(a.a_sq * a.dx * (rxv[h] * rxv[h]),                                                    a.eps + amu[h] * (pxv[h] * pxv[h]));                        const float by = fast_div(a.a_abs * a.dy * fabsf(ryv[h]), a.eps + fabsf(pyv[h]));                 const float sy = fast_div(a.a_sq * a.dy * (ryv[h] * ryv[h]),                                                    a.eps + anu[h] * (pyv[h] * pyv[h]));                        /* NaN candidate -> 0 (numpy minimum + nan_to_num); dx|mu| is finite */                 kx[h] = (bx != bx || sx != sx) ? 0.f : fminf(a.dx * amu[h], fminf(bx, sx));                 ky[h] = (by != by || sy != sy) ? 0.f : fminf(a.dy * anu[h], fminf(by, sy));             }                                                                                     const int64_t o = kb0 + (int64_t)(Y) * g.C;                                           st2(a.kx + o, make_float2(kx[0], kx[1]));                                             st2(a.ky + o, make_float2(ky[0], ky[1]));                                         }                                                                                     if (k_ + P < nsteps) {                                                                    const int is_ = slot + P >= S ? slot + P - S : slot + P;                              st.issue(ya - L + k_ + P, sbase + is_ * SLOTB, FSB, gx_in);                       }                                                                                     cp_async_commit();                                                                    slot = slot + 1 == S ? 0 : slot + 1;                                              }
+#define K2B_STEP(K, KR, OUT, Y)                                                                    \
+{                                                                                                  \
+    const int k_ = (K);                                                                            \
+    cp_async_wait<P - 1>();                                                                        \
+    __syncthreads();                                                                               \
+    const float* buf_ = sm + slot * (NF * FS) + lane;                                              \
+    float2 mx_ = bc2(0.f), my_ = mx_;                                                              \
+    _Pragma("unroll") for (int t = 0; t < T; ++t) {                                                \
+        mx_ = fma2c((float)TP::m(t), ld2(buf_ + t * CC), mx_);                                     \
+        my_ = fma2c((float)TP::m(t), ld2(buf_ + FS + t * CC), my_);                                \
+    }                                                                                              \
+    r2x[(KR)] = mx_;                                                                               \
+    r2y[(KR)] = my_;                                                                               \
+    if ((OUT) && act && (Y) < yb) {                                                                \
+        float2 mmx = bc2(0.f), mmy = mmx;                                                          \
+        _Pragma("unroll") for (int b = 0; b < T; ++b) {                                            \
+            mmx = fma2c((float)TP::m(b), r2x[((KR) + 1 + b) % T], mmx);                            \
+            mmy = fma2c((float)TP::m(b), r2y[((KR) + 1 + b) % T], mmy);                            \
+        }                                                                                          \
+        const int cs_ = slot >= L ? slot - L : slot - L + S;                                       \
+        const float* cb = sm + cs_ * (NF * FS) + L * CC + lane;                                    \
+        const float2 pxc = ld2(cb), pyc = ld2(cb + FS);                                            \
+        const float2 rx = mul2(make_float2(a.alpha_r * mu0, a.alpha_r * mu1), sub2(mmx, pxc));     \
+        const float2 ry = mul2(make_float2(a.alpha_r * nu0, a.alpha_r * nu1), sub2(mmy, pyc));     \
+        const float amu[2] = {fabsf(mu0), fabsf(mu1)}, anu[2] = {fabsf(nu0), fabsf(nu1)};          \
+        const float pxv[2] = {pxc.x, pxc.y}, pyv[2] = {pyc.x, pyc.y};                              \
+        const float rxv[2] = {rx.x, rx.y}, ryv[2] = {ry.x, ry.y};                                  \
+        float kx[2], ky[2];                                                                        \
+        _Pragma("unroll") for (int h = 0; h < 2; ++h) {                                            \
+            const float bx = fast_div(a.a_abs * a.dx * fabsf(rxv[h]), a.eps + fabsf(pxv[h]));      \
+            const float sx = fast_div(a.a_sq * a.dx * (rxv[h] * rxv[h]), a.eps + amu[h] * (pxv[h] * pxv[h])); \
+            const float by = fast_div(a.a_abs * a.dy * fabsf(ryv[h]), a.eps + fabsf(pyv[h]));      \
+            const float sy = fast_div(a.a_sq * a.dy * (ryv[h] * ryv[h]), a.eps + anu[h] * (pyv[h] * pyv[h])); \
+            /* NaN candidate -> 0 (numpy minimum + nan_to_num); dx|mu| is finite */                \
+            kx[h] = (bx != bx || sx != sx) ? 0.f : fminf(a.dx * amu[h], fminf(bx, sx));            \
+            ky[h] = (by != by || sy != sy) ? 0.f : fminf(a.dy * anu[h], fminf(by, sy));            \
+        }                                                                                          \
+        const int64_t o = kb0 + (int64_t)(Y) * g.C;                                                \
+        st2(a.kx + o, make_float2(kx[0], kx[1]));                                                  \
+        st2(a.ky + o, make_float2(ky[0], ky[1]));                                                  \
+    }                                                                                              \
+    if (k_ + P < nsteps) {                                                                         \
+        const int is_ = slot + P >= S ? slot + P - S : slot + P;                                   \
+        st.issue(ya - L + k_ + P, sbase + is_ * SLOTB, FSB, gx_in);                                \
+    }                                                                                              \
+    cp_async_commit();                                                                             \
+    slot = slot + 1 == S ? 0 : slot + 1;                                                           \
+}
 #pragma unroll
     for (int k = 0; k < 2 * L; ++k) K2B_STEP(k, k % T, false, 0);
     int kb = 2 * L;
