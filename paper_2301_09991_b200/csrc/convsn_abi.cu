@@ -420,6 +420,23 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
             return CSN_OK;
         }
     }
+    if constexpr (std::is_same<Real, float>::value) {
+        // single-lane face-uniform kernel: 32-channel CTAs inside one face (odd ng)
+        const int64_t C = (int64_t)g->nd * g->ng;
+        const int64_t face = (int64_t)g->na * g->na * g->ng;
+        if (g_tune_upwind_x2 && n_sweeps == 3 && q_per_dof && a.exact_div == 3 &&
+            C % UPX1_CC == 0 && face % UPX1_CC == 0) {
+            const int gx = (int)cdiv(cdiv(g->ny, UPX_UT), UPX_SPB);
+            const int gy = (int)(C / UPX1_CC);
+            int chunks = (int)cdiv(g->nx, UP_XCHUNK);
+            while (chunks > 1 && (int64_t)gx * gy * (chunks / 2) >= 148 * 8) chunks /= 2;
+            a.xchunk = (int)cdiv(g->nx, chunks);
+            const int gz = (int)cdiv(g->nx, a.xchunk);
+            upwind_smooth_x1_kernel<3><<<dim3(gx, gy, gz), dim3(32, UPX_SPB), 0, st>>>(a);
+            CSN_CHECK_LAUNCH();
+            return CSN_OK;
+        }
+    }
     const int gx = (int)cdiv(cdiv(g->ny, UT), UP_SPB);
     const int gy = (int)cdiv((int64_t)g->nd * g->ng, UP_CC);
     // x chunks: keep chunks long against the H-column warm-up, fill the machine

@@ -377,10 +377,12 @@ def test_checkpoint_resume_bitwise(P, tmp_path, tag, dtype, split):
 
 @pytest.mark.parametrize("nx,ny,na,ng,scale", [(48, 40, 8, 1, 3.0), (32, 38, 8, 2, 1.0),
                                                (40, 24, 4, 4, 3.0), (64, 64, 16, 1, 3.0),
-                                               (36, 44, 32, 1, 1.0), (16, 68, 8, 1, 3.0)])
+                                               (36, 44, 32, 1, 1.0), (16, 68, 8, 1, 3.0),
+                                               (32, 24, 8, 3, 3.0), (24, 20, 4, 7, 1.0)])
 def test_upwind_x2_matches_scalar(P, nx, ny, na, ng, scale):
-    """The packed channel-pair smoother (fp32) is bit-identical to the scalar kernel on
-    every level it takes (face channel count a multiple of 64), incl. ragged strips."""
+    """The face-uniform smoothers (fp32: channel pairs, TMA-staged columns, one channel
+    per lane for odd group counts) are bit-identical to the scalar kernel on every level
+    they take, incl. ragged strips."""
     from paper_2301_09991_b200 import _lib
     rng = np.random.default_rng(7)
     q = P.build_quadrature(na)
