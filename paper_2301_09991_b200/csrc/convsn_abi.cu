@@ -89,6 +89,12 @@ inline int grid1d(int64_t n, int block = 256) {
     return (int)b;
 }
 
+// x chunks of the smoother march: start from 8-column chunks (the H = 3 warm-up columns
+// are then 27% extra work, but small coarse levels need the parallelism: one 64-column
+// chunk per strip left the 128^2 x 128 level at 32 CTAs), then merge chunks while the
+// grid still holds >= 8 CTAs per SM
+inline int up_chunks0(int nx) { return (int)cdiv(nx, 8); }
+
 // rows per CTA chunk for the y-marching kernels: enough CTAs to fill 148 SMs ~4x
 inline int pick_ly(int64_t ctas_xy, int rows, int T) {
     int chunks = 1;
@@ -357,7 +363,7 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
             !(g1 && init_mode == 2 && !a.angle_coarsens)) {
             const int gx = (int)cdiv(cdiv(g->ny, UPX_UT), UPX_SPB);
             const int gy = (int)(C / UPX_CC);
-            int chunks = (int)cdiv(g->nx, UP_XCHUNK);
+            int chunks = up_chunks0(g->nx);
             while (chunks > 1 && (int64_t)gx * gy * (chunks / 2) >= 148 * 8) chunks /= 2;
             a.xchunk = (int)cdiv(g->nx, chunks);
             const int gz = (int)cdiv(g->nx, a.xchunk);
@@ -428,7 +434,7 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
             C % UPX1_CC == 0 && face % UPX1_CC == 0) {
             const int gx = (int)cdiv(cdiv(g->ny, UPX_UT), UPX_SPB);
             const int gy = (int)(C / UPX1_CC);
-            int chunks = (int)cdiv(g->nx, UP_XCHUNK);
+            int chunks = up_chunks0(g->nx);
             while (chunks > 1 && (int64_t)gx * gy * (chunks / 2) >= 148 * 8) chunks /= 2;
             a.xchunk = (int)cdiv(g->nx, chunks);
             const int gz = (int)cdiv(g->nx, a.xchunk);
@@ -440,7 +446,7 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
     const int gx = (int)cdiv(cdiv(g->ny, UT), UP_SPB);
     const int gy = (int)cdiv((int64_t)g->nd * g->ng, UP_CC);
     // x chunks: keep chunks long against the H-column warm-up, fill the machine
-    int chunks = (int)cdiv(g->nx, UP_XCHUNK);
+    int chunks = up_chunks0(g->nx);
     while (chunks > 1 && (int64_t)gx * gy * (chunks / 2) >= 148 * 8) chunks /= 2;
     a.xchunk = (int)cdiv(g->nx, chunks);
     const int gz = (int)cdiv(g->nx, a.xchunk);
