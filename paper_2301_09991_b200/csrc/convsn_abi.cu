@@ -689,6 +689,29 @@ int csn_scalar_flux(int dtype, const csn_geom* g, const void* psi, int halo, con
                     double* phi, void* stream) {
     if (!geom_ok(g) || !psi || !w || !phi || halo < 0) return CSN_E_ARG;
     Geo d = make_geo(*g);
+    if (g->ng <= 8) {      // one warp per cell (coalesced over the cell's channels)
+        const int nb = grid1d((int64_t)g->nx * g->ny * 32);
+        auto run = [&](auto tag) -> int {
+            using Real = decltype(tag);
+            const Real* p = (const Real*)psi;
+            const Real* ww = (const Real*)w;
+            switch (g->ng) {
+                case 1: scalar_flux_cell_kernel<Real, 1><<<nb, 256, 0, S(stream)>>>(d, p, halo, ww, phi); break;
+                case 2: scalar_flux_cell_kernel<Real, 2><<<nb, 256, 0, S(stream)>>>(d, p, halo, ww, phi); break;
+                case 3: scalar_flux_cell_kernel<Real, 3><<<nb, 256, 0, S(stream)>>>(d, p, halo, ww, phi); break;
+                case 4: scalar_flux_cell_kernel<Real, 4><<<nb, 256, 0, S(stream)>>>(d, p, halo, ww, phi); break;
+                case 5: scalar_flux_cell_kernel<Real, 5><<<nb, 256, 0, S(stream)>>>(d, p, halo, ww, phi); break;
+                case 6: scalar_flux_cell_kernel<Real, 6><<<nb, 256, 0, S(stream)>>>(d, p, halo, ww, phi); break;
+                case 7: scalar_flux_cell_kernel<Real, 7><<<nb, 256, 0, S(stream)>>>(d, p, halo, ww, phi); break;
+                default: scalar_flux_cell_kernel<Real, 8><<<nb, 256, 0, S(stream)>>>(d, p, halo, ww, phi); break;
+            }
+            CSN_CHECK_LAUNCH();
+            return CSN_OK;
+        };
+        if (dtype == CSN_F32) return run(float());
+        if (dtype == CSN_F64) return run(double());
+        return CSN_E_DTYPE;
+    }
     const int64_t warps = (int64_t)g->nx * g->ny * g->ng;
     const int nb = grid1d(warps * 32);
     if (dtype == CSN_F32)

@@ -185,6 +185,49 @@ boundary_kernel(Geo g, Real* f, int h, const Real* mu, const Real* nu) {
 }
 
 // ------------------------------------------------------------------ scalar flux
+// one warp per cell, lanes over directions, NG (<= 8) groups per lane: a warp reads its
+// cell's 32 * NG contiguous channels per step (coalesced; the per-(cell, group) warp of
+// scalar_flux_kernel strides by ng), fp64 accumulation in a fixed order (4 partial sums
+// per group for NG == 1), fixed shuffle tree -> deterministic
+template <class Real, int NG>
+__global__ void __launch_bounds__(256)
+scalar_flux_cell_kernel(Geo g, const Real* psi, int h, const Real* w, double* phi) {
+    constexpr int NP = NG == 1 ? 4 : 1;            // partial sums per group
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t ncells = (int64_t)g.nx * g.ny;
+    for (int64_t cell = warp; cell < ncells; cell += nwarps) {
+        const int y = (int)(cell % g.ny), x = (int)(cell / g.ny);
+        const Real* base = psi + fidx(x, y, 0, g.ny, h, g.C);
+        double acc[NG][NP];
+#pragma unroll
+        for (int k = 0; k < NG; ++k)
+#pragma unroll
+            for (int q = 0; q < NP; ++q) acc[k][q] = 0.0;
+        for (int n0 = lane; n0 < g.nd; n0 += 32 * NP) {
+#pragma unroll
+            for (int qq = 0; qq < NP; ++qq) {
+                const int n = n0 + 32 * qq;
+                if (n < g.nd) {
+                    const double wn = (double)w[n];
+                    const Real* pn = base + (int64_t)n * NG;
+#pragma unroll
+                    for (int k = 0; k < NG; ++k) acc[k][qq] = fma(wn, (double)pn[k], acc[k][qq]);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NG; ++k) {
+            double v = acc[k][0];
+#pragma unroll
+            for (int qq = 1; qq < NP; ++qq) v += acc[k][qq];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            if (lane == 0) phi[cell * NG + k] = v;
+        }
+    }
+}
+
 // one warp per (cell, group); fp64 accumulation, fixed shuffle tree.
 template <class Real>
 __global__ void __launch_bounds__(256)
