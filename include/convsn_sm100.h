@@ -64,8 +64,9 @@ const char* csn_error_string(int code);
  *                  b / (s d) with b = the upwind neighbour terms + source, the quotient
  *                  refined by one residual step (the rounded quotient); 4: the same
  *                  without refinement; 2: ce - r / (s d) with the refined quotient;
- *                  1: ce - r / (s d) by IEEE division; 0: one fused ce - r * rcp(s d).
- *                  fp64 always uses the reference form ce - r / (s d).
+ *                  1: ce - r / (s d) by IEEE division; 0: one fused ce - r * rcp(s d)
+ *                  (the face-uniform kernels implement 3 and 0, the other forms run in
+ *                  the scalar kernel).  fp64 always uses the reference form ce - r / (s d).
  *   "sweep_div"  = 1 (default): the fp32 PG sweep refines r / (beta d) the same way;
  *                  0: reciprocal product;
  *   "pg_tma"     = 1 (default): fp32 csn_pg_residual stages padded fields with TMA

@@ -358,7 +358,8 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
         const int64_t C = (int64_t)g->nd * g->ng;
         const int64_t face = (int64_t)g->na * g->na * g->ng;
         const bool g1 = g->ng == 1;
-        if (g_tune_upwind_x2 && n_sweeps == 3 && q_per_dof && C % UPX_CC == 0 &&
+        if (g_tune_upwind_x2 && n_sweeps == 3 && q_per_dof &&
+            (a.exact_div == 3 || a.exact_div == 0) && C % UPX_CC == 0 &&
             face % UPX_CC == 0 && (g1 || g->ng % 2 == 0) &&
             !(g1 && init_mode == 2 && !a.angle_coarsens)) {
             const int gx = (int)cdiv(cdiv(g->ny, UPX_UT), UPX_SPB);
@@ -408,18 +409,12 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
             using T_ = std::true_type;
             using F_ = std::false_type;
             using D0 = std::integral_constant<int, 0>;
-            using D1 = std::integral_constant<int, 1>;
-            using D2 = std::integral_constant<int, 2>;
             using D3 = std::integral_constant<int, 3>;
-            using D4 = std::integral_constant<int, 4>;
+            // packed update forms: 3 (Jacobi, default) and 0 (fused reciprocal); the
+            // other forms run in the scalar kernel
             auto pick = [&](auto g1t) {
-                switch (a.exact_div) {
-                    case 0: go(g1t, D0()); break;
-                    case 1: go(g1t, D1()); break;
-                    case 2: go(g1t, D2()); break;
-                    case 3: go(g1t, D3()); break;
-                    default: go(g1t, D4()); break;
-                }
+                if (a.exact_div == 3) go(g1t, D3());
+                else go(g1t, D0());
             };
             if (g1) pick(T_()); else pick(F_());
             CSN_CHECK_LAUNCH();

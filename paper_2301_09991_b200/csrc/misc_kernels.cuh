@@ -9,8 +9,8 @@ namespace csn {
 // ------------------------------------------------------------------ restriction
 // s_c[I,J,N] = sum_{2x2 cells} sum_{children n of N} r[i,j,n] w_n dxf dyf  (raw),
 // divided by w_N dxc dyc when normalise (R/multigrid.py:326).
-// explicitly rounded products / sums (no contraction), shared with the restriction
-// fused into the fp32 residual kernel (pg_residual_x2_kernel<..., RC = true>)
+// explicitly rounded products / sums / quotients (no contraction: the restriction's
+// rounding does not depend on the compiler's choices)
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
@@ -58,8 +58,7 @@ __global__ void __launch_bounds__(256) restrict_kernel(const RestrictArgs<Real> 
         cf[0] = cc;
         wn[0] = a.wf[N];
     }
-    // 1 / (w_N ac) once per channel (the fused restriction uses the same product)
-    const Real inorm = a.normalise ? div_rn(Real(1), mul_rn(a.wc[N], a.ac)) : Real(1);
+    const Real norm = a.normalise ? mul_rn(a.wc[N], a.ac) : Real(1);
     const Real af = a.af;
     const bool pair = nch == 4 && gf.ng == 1;      // cf[1] == cf[0] + 1, cf[0] even
     const int64_t fpitch = (int64_t)(gf.ny + 2 * a.fine_h) * gf.C;   // x stride (fine)
@@ -101,7 +100,7 @@ __global__ void __launch_bounds__(256) restrict_kernel(const RestrictArgs<Real> 
                 acc = add_rn(acc, sp);
             }
         }
-        if (a.normalise) acc = mul_rn(acc, inorm);
+        if (a.normalise) acc = div_rn(acc, norm);
         a.coarse[fidx(I, J, cc, gc.ny, a.coarse_h, gc.C)] = acc;
     }
 }
