@@ -515,6 +515,18 @@ int csn_apply_boundary(int dtype, const csn_geom* g, void* f, int halo, const vo
     const int64_t cells = (int64_t)2 * halo * (g->ny + 2 * halo) + (int64_t)g->nx * 2 * halo;
     if (cells > INT32_MAX) return CSN_E_ARG;
     // a few CTAs per SM, each looping over halo cells (one cell per CTA is launch-bound)
+    const int64_t face = (int64_t)g->na * g->na * g->ng;
+    if (dtype == CSN_F32 && d.C % 4 == 0 && face % 4 == 0 &&
+        (reinterpret_cast<uintptr_t>(f) & 15) == 0) {
+        const int64_t gx4 = cdiv(d.C / 4, 256);
+        int64_t gy4 = cdiv(148 * 8, gx4);
+        if (gy4 > cells) gy4 = cells;
+        if (gy4 > 65535) gy4 = 65535;
+        boundary4_kernel<<<dim3((unsigned)gx4, (unsigned)(gy4 < 1 ? 1 : gy4)), 256, 0, S(stream)>>>(
+            d, (float*)f, halo, (const float*)mu, (const float*)nu);
+        CSN_CHECK_LAUNCH();
+        return CSN_OK;
+    }
     const int64_t gxb = cdiv(d.C, 256);
     int64_t gyb = cdiv(148 * 8, gxb);
     if (gyb > cells) gyb = cells;
