@@ -360,7 +360,7 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
         const bool g1 = g->ng == 1;
         if (g_tune_upwind_x2 && n_sweeps == 3 && q_per_dof &&
             (a.exact_div == 3 || a.exact_div == 0) && C % UPX_CC == 0 &&
-            face % UPX_CC == 0 && (g1 || g->ng % 2 == 0) &&
+            face % UPX_CC == 0 &&
             !(g1 && init_mode == 2 && !a.angle_coarsens)) {
             const int gx = (int)cdiv(cdiv(g->ny, UPX_UT), UPX_SPB);
             const int gy = (int)(C / UPX_CC);
@@ -402,21 +402,22 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
                 }
                 cudaGetLastError();
             }
-            auto go = [&](auto g1t, auto dmt) {
-                upwind_smooth_x2_kernel<3, decltype(g1t)::value, decltype(dmt)::value>
+            auto go = [&](auto gmt, auto dmt) {
+                upwind_smooth_x2_kernel<3, decltype(gmt)::value, decltype(dmt)::value>
                     <<<grid, block, 0, st>>>(a);
             };
-            using T_ = std::true_type;
-            using F_ = std::false_type;
+            using G0 = std::integral_constant<int, 0>;
+            using G1_ = std::integral_constant<int, 1>;
+            using G2 = std::integral_constant<int, 2>;
             using D0 = std::integral_constant<int, 0>;
             using D3 = std::integral_constant<int, 3>;
             // packed update forms: 3 (Jacobi, default) and 0 (fused reciprocal); the
             // other forms run in the scalar kernel
-            auto pick = [&](auto g1t) {
-                if (a.exact_div == 3) go(g1t, D3());
-                else go(g1t, D0());
+            auto pick = [&](auto gmt) {
+                if (a.exact_div == 3) go(gmt, D3());
+                else go(gmt, D0());
             };
-            if (g1) pick(T_()); else pick(F_());
+            if (g1) pick(G0()); else if (g->ng % 2 == 0) pick(G1_()); else pick(G2());
             CSN_CHECK_LAUNCH();
             return CSN_OK;
         }
