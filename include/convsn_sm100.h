@@ -152,7 +152,11 @@ int64_t csn_pg_workspace_size(int dtype, const csn_geom* g, int order);
  * applies the boundary first (csn_apply_boundary; R/multigrid.py:166,277) and kx, ky are
  * zero outside their +-l band.  fp32 fields padded by >= l (delta too, in the sweep) are
  * staged with TMA as stored; otherwise the kernel re-derives the halo by the vacuum rule
- * — identical for consistent halos (tests/test_gpu_parity.py, tma_residual). */
+ * — identical for consistent halos (tests/test_gpu_parity.py, tma_residual).
+ * dterm (fp32, TMA path only; else CSN_E_SCHEME): unpadded [nx][ny][C] buffer of the k-only
+ * coefficient D = -M_y(kx S_x / 2dx^2) - S_y(ky M_x / 2dy^2) of psi in r.  dterm_mode 1
+ * (residual modes): compute and store it; 2: read it instead of recomputing — valid
+ * while kx, ky are unchanged; results are bit-identical; 0: unused. */
 int csn_pg_residual(int dtype, int order, const csn_geom* g, const double* taps,
                     const void* psi, int psi_halo, const void* delta, int delta_halo,
                     const void* kx, const void* ky, int k_halo,
@@ -160,7 +164,7 @@ int csn_pg_residual(int dtype, int order, const csn_geom* g, const double* taps,
                     const void* mu, const void* nu, const void* strm,
                     void* r, int r_halo, void* psi_out, int psi_out_halo, double beta,
                     double* partials, double* l1, void* avg, int avg_halo, int avg_mode,
-                    double theta, void* stream);
+                    double theta, void* dterm, int dterm_mode, void* stream);
 
 /* R/grid.py:193-198 scalar_flux: phi (device fp64 [nx][ny][ng]) = sum_n w_n psi. */
 int csn_scalar_flux(int dtype, const csn_geom* g, const void* psi, int halo,

@@ -47,7 +47,7 @@ _SIGNATURES = {
     "csn_pg_workspace_size": ([_c_int, _GP, _c_int], _c_i64),
     "csn_pg_residual": ([_c_int, _c_int, _GP, _DP, _vp, _c_int, _vp, _c_int, _vp, _vp, _c_int,
                          _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _c_int, _vp, _c_int, _c_dbl,
-                         _vp, _vp, _vp, _c_int, _c_int, _c_dbl, _vp], _c_int),
+                         _vp, _vp, _vp, _c_int, _c_int, _c_dbl, _vp, _c_int, _vp], _c_int),
     "csn_scalar_flux": ([_c_int, _GP, _vp, _c_int, _vp, _vp, _vp], _c_int),
     "csn_group_source": ([_c_int, _GP, _vp, _vp, _vp, _vp, _c_dbl, _vp, _vp, _vp, _vp], _c_int),
     "csn_fission_source": ([_GP, _vp, _vp, _vp, _c_dbl, _vp, _vp], _c_int),

@@ -140,7 +140,7 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
                      const void* sigma, const void* q, int q_per_dof, const void* mu,
                      const void* nu, const void* strm, void* r, int r_h, void* out, int out_h,
                      double beta, double* partials, double* l1, void* avg, int avg_h, int avg_mode,
-                     double theta, cudaStream_t st) {
+                     double theta, void* dterm, int dterm_mode, cudaStream_t st) {
     constexpr int T = 2 * L + 1;
     if (k_h < L) return CSN_E_ARG;
     if (!taps_match<L>(taps)) return CSN_E_ARG;
@@ -159,6 +159,7 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
     a.r = (Real*)r; a.r_h = r_h;
     a.out = (Real*)out; a.out_h = out_h; a.beta = (Real)beta;
     a.refine_div = g_tune_sweep_div;
+    a.dterm = (Real*)dterm;
     // fp32: packed-fp32x2 kernel, a lane per channel pair (64 channels per CTA)
     constexpr bool X2 = sizeof(Real) == 4;
     const int gx = (int)cdiv(g->nx, PG_TX);
@@ -180,11 +181,22 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
                          (out ? field_map(&maps.aux, delta, g, delta_h, W)
                               : (!a.avg_mode || field_map(&maps.aux, avg, g, avg_h, PG_TX)));
         if (!tma) cudaGetLastError();
+        if (dterm_mode && !tma) return CSN_E_SCHEME;      // the stored D needs the TMA kernel
         if (tma) {
             if (!out && l1 && !partials) return CSN_E_ARG;
-            if (out) launch_pg_resid_tma<L, PG_SWEEP>(grid, block, st, a, maps);
-            else if (a.avg_mode) launch_pg_resid_tma<L, PG_RESID_EMA>(grid, block, st, a, maps);
-            else launch_pg_resid_tma<L, PG_RESID>(grid, block, st, a, maps);
+            if (out) {
+                if (dterm_mode == 2) launch_pg_resid_tma<L, PG_SWEEP, 2>(grid, block, st, a, maps);
+                else if (dterm_mode == 0) launch_pg_resid_tma<L, PG_SWEEP, 0>(grid, block, st, a, maps);
+                else return CSN_E_SCHEME;
+            } else if (a.avg_mode) {
+                if (dterm_mode == 1) launch_pg_resid_tma<L, PG_RESID_EMA, 1>(grid, block, st, a, maps);
+                else if (dterm_mode == 2) launch_pg_resid_tma<L, PG_RESID_EMA, 2>(grid, block, st, a, maps);
+                else launch_pg_resid_tma<L, PG_RESID_EMA, 0>(grid, block, st, a, maps);
+            } else {
+                if (dterm_mode == 1) launch_pg_resid_tma<L, PG_RESID, 1>(grid, block, st, a, maps);
+                else if (dterm_mode == 2) launch_pg_resid_tma<L, PG_RESID, 2>(grid, block, st, a, maps);
+                else launch_pg_resid_tma<L, PG_RESID, 0>(grid, block, st, a, maps);
+            }
             CSN_CHECK_LAUNCH();
             if (!out && l1) {
                 sum_f64_kernel<<<1, 1024, 0, st>>>(partials, (int64_t)gx * gy * gz, 1.0, l1);
@@ -683,14 +695,16 @@ int csn_pg_residual(int dtype, int order, const csn_geom* g, const double* taps,
                     int q_per_dof, const void* mu, const void* nu, const void* strm, void* r,
                     int r_halo, void* psi_out, int psi_out_halo, double beta, double* partials,
                     double* l1, void* avg, int avg_halo, int avg_mode, double theta,
-                    void* stream) {
+                    void* dterm, int dterm_mode, void* stream) {
     if (!geom_ok(g) || !taps || !psi || !kx || !ky || !sigma || !q || !mu || !nu)
+        return CSN_E_ARG;
+    if (dterm_mode < 0 || dterm_mode > 2 || (dterm_mode && (!dterm || dtype != CSN_F32)))
         return CSN_E_ARG;
     if (psi_out && (!strm || psi_out == psi)) return CSN_E_ARG;
     if (dtype != CSN_F32 && dtype != CSN_F64) return CSN_E_DTYPE;
     ORDER_DISPATCH(pg_residual_impl, g, taps, psi, psi_halo, delta, delta_halo, kx, ky, k_halo,
                    sigma, q, q_per_dof, mu, nu, strm, r, r_halo, psi_out, psi_out_halo, beta,
-                   partials, l1, avg, avg_halo, avg_mode, theta, S(stream));
+                   partials, l1, avg, avg_halo, avg_mode, theta, dterm, dterm_mode, S(stream));
 }
 
 int csn_scalar_flux(int dtype, const csn_geom* g, const void* psi, int halo, const void* w,

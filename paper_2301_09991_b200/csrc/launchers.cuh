@@ -27,13 +27,13 @@ void launch_pg_resid_x2(dim3 grid, dim3 block, cudaStream_t st, const PGResidArg
     pg_residual_x2_kernel<L, MODE, VEC><<<grid, block, sm, st>>>(a);
 }
 
-template <int L, int MODE>
+template <int L, int MODE, int KD>
 void launch_pg_resid_tma(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<float>& a,
                          const PGTmaMaps& maps) {
     constexpr size_t sm = pg_residual_tma_smem<L, MODE>();
     static bool attr = false;
-    if (!attr) { set_smem(pg_residual_tma_kernel<L, MODE>, sm); attr = true; }
-    pg_residual_tma_kernel<L, MODE><<<grid, block, sm, st>>>(a, maps);
+    if (!attr) { set_smem(pg_residual_tma_kernel<L, MODE, KD>, sm); attr = true; }
+    pg_residual_tma_kernel<L, MODE, KD><<<grid, block, sm, st>>>(a, maps);
 }
 
 template <int L, bool EMA, int VEC>

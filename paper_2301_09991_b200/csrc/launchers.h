@@ -16,7 +16,7 @@ template <class Real, int L, int MODE, int VEC>
 void launch_pg_resid(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<Real>& a);
 template <int L, int MODE, int VEC>
 void launch_pg_resid_x2(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<float>& a);
-template <int L, int MODE>
+template <int L, int MODE, int KD>
 void launch_pg_resid_tma(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<float>& a,
                          const PGTmaMaps& maps);
 template <int L, bool EMA, int VEC>

@@ -68,6 +68,10 @@ struct PGResidArgs {
     Real* avg; int avg_h; int avg_mode; Real theta, omt;   // fused EMA (frozen cycles)
     int ly;             // y rows per CTA chunk, multiple of T
     int refine_div;     // fp32 sweep: refine r / (beta d) to the rounded quotient
+    // k-only term D = -M_y(hx S_x kx) - S_y(hy M_x ky) of the residual (the coefficient
+    // of psi at the output cell), unpadded [nx][ny][C]: written (KD 1) by the residual
+    // after a diffusivity refresh, read (KD 2) while k is unchanged (TMA kernel)
+    Real* dterm;
 };
 
 // residual kernel modes: plain residual, residual + fused iterate EMA, fused sweep

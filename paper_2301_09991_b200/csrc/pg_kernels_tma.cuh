@@ -45,9 +45,11 @@ constexpr size_t pg_residual_tma_smem() {
            128;   // + alignment slack (TMA destinations: 128 B)
 }
 
-template <int L, int MODE>
+template <int L, int MODE, int KD = 0>
 __global__ void __launch_bounds__(32 * PG_TX, L <= 3 ? 2 : 1)
 pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTmaMaps m) {
+    // KD 0: D computed here; 1: computed and stored to a.dterm; 2: read from a.dterm
+    // (bit-identical: the stored value is the one this kernel would compute)
     constexpr bool SWEEP = MODE == PG_SWEEP;
     constexpr bool EMA = MODE == PG_RESID_EMA;
     using TP = UnitTaps<L>;
@@ -56,7 +58,7 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
     constexpr int W = PG_TX + 2 * L;
     constexpr int NF = MODE == PG_RESID ? 3 : 4;
     constexpr int S = TmaRing<L, MODE>::S;
-    constexpr int P = S - L - 1;
+    constexpr int P = TmaRing<L, MODE>::PREFETCH;   // (S - L - 1)
     constexpr int FS = W * CC;                     // floats per field row
     constexpr int SLOT = TmaRing<L, MODE>::SLOT;
     constexpr unsigned ROWB = W * CC * sizeof(float);
@@ -129,6 +131,9 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
     float2 rA[T], rB[T], rC[T], rD[T];              // pending outputs, by (y - ya) mod T
 #pragma unroll
     for (int i = 0; i < T; ++i) rA[i] = rB[i] = rC[i] = rD[i] = bc2(0.f);
+    float* dt_p = KD ? a.dterm + fidx(xs, 0, cs, g.ny, 0, g.C) : nullptr;
+    float2 dN = bc2(0.f);
+    if (KD == 2 && act) dN = ld2(dt_p + (int64_t)ya * g.C);
 
     if (producer) {
 #pragma unroll
@@ -147,10 +152,11 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
 #define TMA_STEP(K, SK, OUT, Y)                                                       \
     {                                                                                 \
         const int k_ = (K);                                                           \
-        float2 sg_ = sgN, q_ = qN;                                                    \
+        float2 sg_ = sgN, q_ = qN, dd_ = dN;                                          \
         if ((OUT) && act && (Y) + 1 < yb) {                                           \
             sgN = make_float2(sig0[((Y) + 1) * g.ng], sig1[((Y) + 1) * g.ng]);       \
             qN = make_float2(q0[((Y) + 1) * qst], q1[((Y) + 1) * qst]);              \
+            if (KD == 2) dN = ld2(dt_p + (int64_t)((Y) + 1) * g.C);                  \
         }                                                                             \
         mbar_wait(&full[slot], fpar);                                                 \
         const float* buf_ = sm + slot * SLOT;                                         \
@@ -179,9 +185,9 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
                 a_m = fma2c((float)TP::m(t_), p_, a_m);                               \
                 a_s = fma2c((float)TP::s(t_), p_, a_s);                               \
                 a_sk = fma2c((float)TP::s(t_), mul2(p_, k1_), a_sk);                  \
-                a_k = fma2c((float)TP::s(t_), k1_, a_k);                              \
+                if (KD != 2) a_k = fma2c((float)TP::s(t_), k1_, a_k);                 \
                 a_mk = fma2c((float)TP::m(t_), mul2(p_, k2_), a_mk);                  \
-                a_ky = fma2c((float)TP::m(t_), k2_, a_ky);                            \
+                if (KD != 2) a_ky = fma2c((float)TP::m(t_), k2_, a_ky);               \
             }                                                                         \
         }                                                                             \
         const float2 xa_ = fma2(mu_dx, a_g, mul2(hx, a_sk));                          \
@@ -197,12 +203,12 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
                 rA[sl_] = fma2c(m_, xa_, fma2c(gt_, xg_, mul2(bc2(s_), xs_)));        \
                 rB[sl_] = mul2(bc2(m_), a_s);                                         \
                 rC[sl_] = mul2(bc2(s_), a_m);                                         \
-                rD[sl_] = fma2c(m_, xd1_, mul2(bc2(s_), xd2_));                       \
+                if (KD != 2) rD[sl_] = fma2c(m_, xd1_, mul2(bc2(s_), xd2_));          \
             } else {                                                                  \
                 rA[sl_] = fma2c(m_, xa_, fma2c(gt_, xg_, fma2c(s_, xs_, rA[sl_])));   \
                 rB[sl_] = fma2c(m_, a_s, rB[sl_]);                                    \
                 rC[sl_] = fma2c(s_, a_m, rC[sl_]);                                    \
-                rD[sl_] = fma2c(m_, xd1_, fma2c(s_, xd2_, rD[sl_]));                  \
+                if (KD != 2) rD[sl_] = fma2c(m_, xd1_, fma2c(s_, xd2_, rD[sl_]));     \
             }                                                                         \
         }                                                                             \
         const int cs_ = slot >= L ? slot - L : slot - L + S;  /* centre row's slot */ \
@@ -214,7 +220,9 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
             const float2 kxc_ = ld2(cb_ + FS), kyc_ = ld2(cb_ + 2 * FS);             \
             float2 r_ = fma2(hx, mul2(kxc_, rB[SK]), rA[SK]);                         \
             r_ = fma2(hy, mul2(kyc_, rC[SK]), r_);                                    \
-            r_ = sub2(fma2(pc_, add2(rD[SK], sg_), r_), q_);                          \
+            const float2 dk_ = KD == 2 ? dd_ : rD[SK];                                \
+            if (KD == 1) st2(dt_p + (int64_t)y_ * g.C, dk_);                         \
+            r_ = sub2(fma2(pc_, add2(dk_, sg_), r_), q_);                             \
             if (SWEEP) {                                                              \
                 const float2 d_ = mul2(beta2, add2(strm2, sg_));                      \
                 const float2 inv_ = make_float2(rcp_nr(d_.x), rcp_nr(d_.y));          \

@@ -21,9 +21,9 @@ CSN_K64(false, 1) CSN_K64(false, 2) CSN_K64(true, 1) CSN_K64(true, 2)
 #else
 #define CSN_RES32(M, V) template void launch_pg_resid_x2<CSN_L, M, V>(CSN_ARGS_R(float));
 CSN_RES32(0, 1) CSN_RES32(0, 4) CSN_RES32(1, 1) CSN_RES32(1, 4) CSN_RES32(2, 1) CSN_RES32(2, 4)
-#define CSN_TMA(M) \
-    template void launch_pg_resid_tma<CSN_L, M>(CSN_ARGS_R(float), const PGTmaMaps&);
-CSN_TMA(0) CSN_TMA(1) CSN_TMA(2)
+#define CSN_TMA(M, KD) \
+    template void launch_pg_resid_tma<CSN_L, M, KD>(CSN_ARGS_R(float), const PGTmaMaps&);
+CSN_TMA(0, 0) CSN_TMA(0, 1) CSN_TMA(0, 2) CSN_TMA(1, 0) CSN_TMA(1, 1) CSN_TMA(1, 2) CSN_TMA(2, 0) CSN_TMA(2, 2)
 #if CSN_L <= 3
 #define CSN_K32(E, V)                                                                  \
     template void launch_pg_k_x2<CSN_L, E, V>(CSN_ARGS_K(float));                     \

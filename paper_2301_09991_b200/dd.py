@@ -213,6 +213,7 @@ class DDCycleEngine(CycleEngine):
         self.x0_levels = x0_levels
         super().__init__(local_h, n_group, dtype, device)
         self.pad_delta = False         # x-ghosted finest correction (see correction)
+        self.use_dterm = False
         west, east = comm.rank > 0, comm.rank < comm.size - 1
         self.geoms = [lev.geom(n_group, int(west), int(east)) for lev in local_h.levels]
         self.sigma = sigma_ghosted

@@ -177,7 +177,7 @@ def pg_residual(psi, mat, q, quad, fs, cfg, diffusivities=None, anisotropy="xy")
 def pg_residual_launch(psi, mat, q, quad, fs, kx, ky, k_halo, r=None, r_halo=0, psi_out=None,
                        out_halo=0, delta=None, delta_halo=0, beta=1.0, partials=None, l1=None,
                        sigma=None, qt=None, per_dof=None, consts=None, avg=None, avg_mode=0,
-                       theta=1.0, gm=None):
+                       theta=1.0, gm=None, dterm=None, dterm_mode=0):
     d = psi.data
     g = psi.grid
     if sigma is None:
@@ -192,7 +192,8 @@ def pg_residual_launch(psi, mat, q, quad, fs, kx, ky, k_halo, r=None, r_halo=0, 
               _lib.ptr(delta), delta_halo, _lib.ptr(kx), _lib.ptr(ky), k_halo, _lib.ptr(sigma),
               _lib.ptr(qt), per_dof, _lib.ptr(qd["mu"]), _lib.ptr(qd["nu"]), _lib.ptr(qd["strm"]),
               _lib.ptr(r), r_halo, _lib.ptr(psi_out), out_halo, float(beta), _lib.ptr(partials),
-              _lib.ptr(l1), _lib.ptr(avg), g.halo, int(avg_mode), float(theta), _lib.stream())
+              _lib.ptr(l1), _lib.ptr(avg), g.halo, int(avg_mode), float(theta), _lib.ptr(dterm),
+              int(dterm_mode), _lib.stream())
 
 
 def pg_isotropic_diffusivity(psi, fs, quad, cfg, mode="mixed_mass", grads=None):

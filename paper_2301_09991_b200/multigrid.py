@@ -12,6 +12,7 @@ residual read-back that drives ``PGState``.
 """
 
 import gc
+import itertools
 import numpy as np
 import torch
 
@@ -252,6 +253,10 @@ _UNFREEZE_GROWTH = 2.0
 _MAX_FREEZE_ATTEMPTS = 3
 
 
+# versions of PGState diffusivities (never reused): keys the engine's stored k-term D
+_K_VERSIONS = itertools.count(1)
+
+
 class PGState:
     """Across-cycle diffusivity Picard state (R/multigrid.py:185-256).
 
@@ -262,7 +267,7 @@ class PGState:
 
     __slots__ = ("diffusivities", "initial_residual", "frozen", "best_residual",
                  "cycles_since_best", "freeze_residual", "failed_freezes", "avg_theta",
-                 "_avg", "_avg_spare", "_avg_grid", "_avg_quad", "log", "_calls")
+                 "_avg", "_avg_spare", "_avg_grid", "_avg_quad", "log", "_calls", "k_version")
 
     def __init__(self, avg_theta=0.2):
         self.diffusivities = None
@@ -279,6 +284,7 @@ class PGState:
         self._avg_quad = None
         self.log = []
         self._calls = 0
+        self.k_version = next(_K_VERSIONS)   # changes whenever the diffusivities do
 
     @property
     def psi_avg(self):
@@ -374,6 +380,7 @@ class PGState:
         self._avg_grid, self._avg_quad = grid, quad
         self.diffusivities = None if d["kx"] is None else (dev(d["kx"]).contiguous(),
                                                            dev(d["ky"]).contiguous())
+        self.k_version = next(_K_VERSIONS)
 
     def scale_average(self, s):
         """psi_avg /= s (R/eigen.py:246-247)."""
@@ -421,12 +428,19 @@ class CycleEngine:
         self._seen = set()
         self._cap_stream = None
         self._graph_warm = False
-        # pad_delta: the finest correction goes to a padded buffer whose halo gets the
-        # boundary rule, so the fp32 sweep takes the TMA kernel (psi - delta formed at
-        # each read).  Off: measured on C4 the TMA sweep is 2% slower than the cp.async
-        # sweep (which forms psi - delta once per staged item) plus the delta boundary
-        self.pad_delta = False
+        # use_dterm (fp32): the residual stores the k-only coefficient D of psi whenever
+        # the diffusivities change and the frozen-cycle residual and the sweep read it
+        # (csn_pg_residual dterm_mode; bit-identical).  The sweep then runs in the TMA
+        # kernel, which needs the finest correction padded with its boundary applied
+        # (pad_delta: psi - delta is formed at each read).  Off by default: on C4 it
+        # removes 23% of the sweep's FMAs but the cycle is unchanged (11.03 vs 11.04 ms:
+        # K5 -2%, K3E -3%, K3 +5% for the D write, +0.03 ms delta boundary) — the PG
+        # kernels are latency-bound at 16 warps/SM, not FMA-bound.
+        self.use_dterm = False
+        self.pad_delta = self.use_dterm
         self.delta0p = None
+        self.dterm = None
+        self._dkey = None
 
     def _t0(self):
         if self.probe is None:
@@ -601,8 +615,20 @@ class CycleEngine:
                             pg_state._avg_spare = torch.empty_like(d)
                         plan["k2"] = (pg_state._avg, pg_state._avg_spare, 2, theta)
                         plan["swap_avg"] = True
+        plan["kd3"], plan["kd5"], plan["dkey"] = 0, 0, None
+        if scheme == "pg" and self.use_dterm:
+            if self.dterm is None or self.dterm.shape != (psi.grid.nx, psi.grid.ny) + d.shape[2:]:
+                self.dterm = torch.empty((psi.grid.nx, psi.grid.ny) + d.shape[2:], dtype=d.dtype,
+                                         device=d.device)
+                self._dkey = None
+            live = plan["k2"] is not None
+            ver = None if pg_state is None else pg_state.k_version
+            key = (plan["kx"].data_ptr(), plan["ky"].data_ptr(), ver)
+            plan["kd3"] = 2 if (not live and self._dkey == key) else 1
+            plan["kd5"] = 2
+            plan["dkey"] = live
         ema, k2 = plan["ema"], plan["k2"]
-        plan["key"] = (d.data_ptr(), self.psi_alt.data_ptr(),
+        plan["key"] = (d.data_ptr(), self.psi_alt.data_ptr(), plan["kd3"], plan["kd5"],
                        None if plan["kx"] is None else plan["kx"].data_ptr(),
                        None if k2 is None else tuple(None if t is None or isinstance(t, (int, float))
                                                      else t.data_ptr() for t in k2[:2]) + k2[2:],
@@ -641,7 +667,8 @@ class CycleEngine:
             pg_residual_launch(view, None, None, f.quad, fs, kx, ky, g.halo, r=self.r0, r_halo=0,
                                partials=self.partials, l1=self.l1, sigma=self.sigma[0], qt=qt,
                                per_dof=per_dof, consts=c0, avg=ema[0], avg_mode=ema[1],
-                               theta=ema[2], gm=self.geoms[0])
+                               theta=ema[2], gm=self.geoms[0], dterm=self.dterm,
+                               dterm_mode=plan["kd3"])
             self._t1("pg_residual" if ema[1] == 0 else "pg_residual+ema", t)
         else:
             t = self._t0()
@@ -673,7 +700,8 @@ class CycleEngine:
                                    psi_out=bufs[(k + 1) % 2], out_halo=g.halo,
                                    delta=delta if k == 0 else None, delta_halo=dh,
                                    beta=cfg.beta_diag, sigma=self.sigma[0], qt=qt,
-                                   per_dof=per_dof, consts=c0, gm=self.geoms[0])
+                                   per_dof=per_dof, consts=c0, gm=self.geoms[0],
+                                   dterm=self.dterm, dterm_mode=plan["kd5"] if k == 0 else 0)
                 self._t1("pg_sweep", t)
             view.data = bufs[plan["pg_sweeps"] % 2]
         else:
@@ -685,7 +713,13 @@ class CycleEngine:
         self._t1("boundary", t)
 
     def _commit(self, plan, psi, pg_state):
-        """Host bookkeeping after the launches: ping-pong buffer ownership."""
+        """Host bookkeeping after the launches: ping-pong buffer ownership, the version of
+        the diffusivities the stored k-term D belongs to."""
+        if plan["k2"] is not None and pg_state is not None:
+            pg_state.k_version = next(_K_VERSIONS)
+        if plan["kd3"] == 1:
+            self._dkey = (plan["kx"].data_ptr(), plan["ky"].data_ptr(),
+                          None if pg_state is None else pg_state.k_version)
         if plan["pg_sweeps"] % 2 == 1:
             psi.data, self.psi_alt = plan["alt"], plan["psi"]
         if plan.get("swap_avg"):

@@ -503,3 +503,29 @@ def test_split_diffusivities_match_fused(P, nx, ny, na, ng, p):
         assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1]), mode
         if mode:
             assert torch.equal(out[0][2], out[1][2]), mode
+
+
+@pytest.mark.parametrize("tag", ["c2_reduced", "c3_reduced"])
+def test_stored_dterm_bitwise(P, tag):
+    """Cycles with the stored k-term D (frozen-cycle residual and sweep read it, the
+    refreshing residual writes it) reproduce the recomputing cycles bit for bit."""
+    from paper_2301_09991_b200 import benchmarks as B, eigen as E
+    from paper_2301_09991_b200.problems import problem_from_data
+    pd = DRIVERS[tag][0](B)
+    o = dict(pd.options)
+    pg = o.pop("pg", None)
+    opts = P.SolverOptions(**o, pg=P.PGConfig(**(pg or {})), dtype="float32")
+    prob = problem_from_data(pd)
+    out = []
+    for use in (True, False):
+        s = E.Solver(prob, opts, inner_iters=getattr(pd, "inner_iters", None))
+        s.eng.use_dterm = use
+        s.eng.pad_delta = use
+        for _ in range(12):
+            if s.done:
+                break
+            s.step()
+        torch.cuda.synchronize()
+        out.append((s.psi.data.clone(), list(s.history), list(s.pgs.log)))
+    assert torch.equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1] and out[0][2] == out[1][2]
