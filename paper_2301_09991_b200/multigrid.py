@@ -646,7 +646,12 @@ class CycleEngine:
         view.grid = g
         view.data = psi_in
         nd, ng, na = psi_in.shape[2], psi_in.shape[3], f.quad.n_a
-        reach = 3 * fs.half_width if scheme == "pg" else 1
+        # x reach of the kernels reading psi: the diffusivity refresh needs 3l (EMA'd
+        # iterate -> gradients on +-2l -> mass pass), the residual and sweep l
+        if scheme == "pg":
+            reach = (3 if plan["k2"] is not None else 1) * fs.half_width
+        else:
+            reach = 1
         self._hook_exchange("psi", psi_in, reach)
         if scheme == "pg":
             kx, ky = plan["kx"], plan["ky"]
