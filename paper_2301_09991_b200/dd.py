@@ -82,21 +82,17 @@ class TorchDistComm(SlabComm):
             return
         dist = self.dist
         we, ee, wg, eg = _edges(t, width, hx)
-        ops, recv = [], []
+        # x is the slowest axis of a contiguous field: every band is one contiguous block,
+        # sent from and received into place
+        ops = []
         if self.rank > 0:
-            buf = torch.empty_like(wg)
-            ops += [dist.P2POp(dist.isend, we.contiguous(), self.rank - 1, self.group),
-                    dist.P2POp(dist.irecv, buf, self.rank - 1, self.group)]
-            recv.append((wg, buf))
+            ops += [dist.P2POp(dist.isend, we, self.rank - 1, self.group),
+                    dist.P2POp(dist.irecv, wg, self.rank - 1, self.group)]
         if self.rank < self.size - 1:
-            buf = torch.empty_like(eg)
-            ops += [dist.P2POp(dist.isend, ee.contiguous(), self.rank + 1, self.group),
-                    dist.P2POp(dist.irecv, buf, self.rank + 1, self.group)]
-            recv.append((eg, buf))
+            ops += [dist.P2POp(dist.isend, ee, self.rank + 1, self.group),
+                    dist.P2POp(dist.irecv, eg, self.rank + 1, self.group)]
         for req in dist.batch_isend_irecv(ops):
             req.wait()
-        for dst, buf in recv:
-            dst.copy_(buf)
 
     def allreduce_sum_(self, t):
         if self.size > 1:
@@ -245,13 +241,14 @@ class DDCycleEngine(CycleEngine):
         L = self.h.levels
         dt = _lib.dtype_code(r0)
         comm = self.comm
-        # local restriction down the distributed levels; ghosts for the smoother warm-up
-        comm.exchange(self.src_g[0].full, GX, GX)
+        # local restriction down the distributed levels; source ghosts for the smoother's
+        # H-column warm-up
+        comm.exchange(self.src_g[0].full, UP_MAX_SWEEPS, GX)
         for i in range(1, len(L)):
             _lib.call("csn_restrict", dt, self.geoms[i - 1], self.geoms[i],
                       _lib.ptr(self.src[i - 1]), 0, _lib.ptr(self.consts[i - 1]["w"]),
                       _lib.ptr(self.consts[i]["w"]), 1, _lib.ptr(self.src[i]), 0, _lib.stream())
-            comm.exchange(self.src_g[i].full, GX, GX)
+            comm.exchange(self.src_g[i].full, UP_MAX_SWEEPS, GX)
         # gathered coarse hierarchy: restrict the last distributed level onto the coarse
         # level's slab, gather, solve redundantly
         cl = self.coarse_h.levels[0]
@@ -274,7 +271,10 @@ class DDCycleEngine(CycleEngine):
             scale = finest_scale if i == 0 else 1.0
             prev = _smooth_chain(L[i], self.ng, self.src[i], 1, prev, 2, 0, gc, n_sweeps, scale,
                                  self.delta[i], 0, None, self.sigma[i], self.geoms[i])
-            comm.exchange(self.delta_g[i].full, GX, GX)
+            # ghosts the next reader needs: the finer level's warm-up prolongs from
+            # (H + 1) / 2 coarse columns; the fused sweep reads l columns of the finest
+            w = (UP_MAX_SWEEPS + 1) // 2 if i > 0 else min(GX, self.sweep_reach)
+            comm.exchange(self.delta_g[i].full, w, GX)
             gc = self.geoms[i]
         return prev
 

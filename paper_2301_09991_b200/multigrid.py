@@ -439,6 +439,7 @@ class CycleEngine:
         self.use_dterm = False
         self.pad_delta = self.use_dterm
         self.delta0p = None
+        self.sweep_reach = 1
         self.dterm = None
         self._dkey = None
 
@@ -684,6 +685,7 @@ class CycleEngine:
             self._t1("upwind_residual", t)
         self._hook_l1()
         self.res_host.copy_(self.l1, non_blocking=True)
+        self.sweep_reach = fs.half_width if scheme == "pg" else 1    # x reach of the update
         pad = self.pad_delta and plan["pg_sweeps"] > 0
         dh = fs.half_width if pad else 0
         if pad and (self.delta0p is None or self.delta0p.shape[0] != g.nx + 2 * dh):
