@@ -71,6 +71,8 @@ const char* csn_error_string(int code);
  *                  0: reciprocal product;
  *   "pg_tma"     = 1 (default): fp32 csn_pg_residual stages padded fields with TMA
  *                  (mbarrier ring); 0 forces the cp.async kernel (bit-identical);
+ *   "k2_tma"     = 1 (default): the fp32 diffusivity path's second pass (k from the
+ *                  workspace) stages rows with TMA; 0: cp.async (bit-identical);
  *   "upwind_tma" = 0 (default): 1 stages the packed smoother's columns with TMA where
  *                  the layout allows (bit-identical; measured 3% slower on C4).
  * The previous value is stored in *prev (nullable). */

@@ -25,6 +25,7 @@ int g_tune_upwind_div = 3;
 int g_tune_sweep_div = 1;
 int g_tune_pg_tma = 1;
 int g_tune_upwind_tma = 0;
+int g_tune_k2_tma = 1;
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -297,8 +298,14 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
             const int gx = (int)cdiv(g->nx + 2 * L, PG_TX);
             a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T);
             dim3 grid(gx, gy, (int)cdiv(g->ny + 2 * L, a.ly));
-            if (vec) launch_pg_kcoef_x2<L, V>(grid, block, st, a, gxp, gyp, gh);
+            // TMA staging of the workspace rows (k2_tma), else the cp.async stager
+            KcoefMaps km;     // the workspace is a field with halo gh = 2l
+            const bool tk = g_tune_k2_tma && field_map(&km.gx, gxp, g, gh, PG_TX + 2 * L) &&
+                            field_map(&km.gy, gyp, g, gh, PG_TX + 2 * L);
+            if (tk) launch_pg_kcoef_tma<L>(grid, block, st, a, km, gh);
+            else if (vec) launch_pg_kcoef_x2<L, V>(grid, block, st, a, gxp, gyp, gh);
             else launch_pg_kcoef_x2<L, 1>(grid, block, st, a, gxp, gyp, gh);
+            if (!tk) cudaGetLastError();
             CSN_CHECK_LAUNCH();
         }
         return CSN_OK;
@@ -489,6 +496,7 @@ int csn_set_tuning(const char* key, int value, int* prev) {
     if (!strcmp(key, "sweep_div")) slot = &g_tune_sweep_div;
     if (!strcmp(key, "pg_tma")) slot = &g_tune_pg_tma;
     if (!strcmp(key, "upwind_tma")) slot = &g_tune_upwind_tma;
+    if (!strcmp(key, "k2_tma")) slot = &g_tune_k2_tma;
     if (!slot) return CSN_E_ARG;
     if (prev) *prev = *slot;
     *slot = value;

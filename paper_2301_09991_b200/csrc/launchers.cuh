@@ -36,6 +36,15 @@ void launch_pg_resid_tma(dim3 grid, dim3 block, cudaStream_t st, const PGResidAr
     pg_residual_tma_kernel<L, MODE, KD><<<grid, block, sm, st>>>(a, maps);
 }
 
+template <int L>
+void launch_pg_kcoef_tma(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a,
+                         const KcoefMaps& maps, int gh) {
+    constexpr size_t sm = pg_kcoef_tma_smem<L>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_kcoef_tma_kernel<L>, sm); attr = true; }
+    pg_kcoef_tma_kernel<L><<<grid, block, sm, st>>>(a, maps, gh);
+}
+
 template <int L, bool EMA, int VEC>
 void launch_pg_k_x2(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a) {
     constexpr size_t sm = pg_k_x2_smem<L, EMA>();

@@ -266,3 +266,144 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
 }
 
 }  // namespace csn
+
+namespace csn {
+
+// ---------------------------------------------------------------------------------
+// K2b (pg_kcoef_x2_kernel) with TMA row staging: R = alpha mu (M_y M_x psi_x - psi_x)
+// and k on the +-l band from the K2a workspace (psi_x, psi_y on the +-2l band, halo 2l,
+// read as stored; boxes beyond it are zero-filled like the cp.async stager's band
+// rule).  Same lane mapping, passes and k formula (k_coef): bit-identical k.  K2b is
+// issue-bound, so the per-thread staging work the TMA producer removes is time saved.
+// ---------------------------------------------------------------------------------
+struct KcoefMaps {
+    CUtensorMap gx, gy;
+};
+
+template <int L>
+constexpr size_t pg_kcoef_tma_smem() {
+    return (size_t)X2Stages<L>::value * 2 * (PG_TX + 2 * L) * X2_CC * sizeof(float) + 128;
+}
+
+template <int L>
+__global__ void __launch_bounds__(32 * PG_TX, 3)
+pg_kcoef_tma_kernel(const PGKArgs<float> a, const __grid_constant__ KcoefMaps m, int gh) {
+    using TP = UnitTaps<L>;
+    constexpr int T = 2 * L + 1;
+    constexpr int CC = X2_CC;
+    constexpr int W = PG_TX + 2 * L;
+    constexpr int S = X2Stages<L>::value;
+    constexpr int P = S - L - 1;
+    constexpr int FS = W * CC;
+    constexpr int SLOT = 2 * FS;
+    constexpr unsigned TXB = 2 * FS * sizeof(float);
+    extern __shared__ __align__(128) unsigned char smraw[];
+    float* sm = reinterpret_cast<float*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
+    __shared__ __align__(8) uint64_t full[S], empty[S];
+
+    const Geo& g = a.g;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = ty * 32 + tx;
+    const int c0 = blockIdx.y * CC;
+    const int c = c0 + 2 * tx;
+    const bool cval = c < g.C;
+    const int cs = cval ? c : g.C - 2;
+    const int n0 = cs / g.ng, n1 = (cs + 1) / g.ng;
+    const float mu0 = a.mu[n0], mu1 = a.mu[n1], nu0 = a.nu[n0], nu1 = a.nu[n1];
+    const int x0 = -L + (int)blockIdx.x * PG_TX;             // band x in [-l, nx+l)
+    const int x = x0 + ty;
+    const bool act = x < g.nx + L && cval;
+    const int ya = -L + (int)blockIdx.z * a.ly;              // band y in [-l, ny+l)
+    const int yb = min(g.ny + L, ya + a.ly);
+    const int nsteps = 2 * L + (int)(((yb - ya) + T - 1) / T) * T;
+    const int64_t kb0 = fidx(act ? x : 0, 0, cs, g.ny, a.k_h, g.C);
+    const int lane = ty * CC + 2 * tx;
+    const bool producer = tid == 0;
+
+    if (producer) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], PG_TX);
+        }
+        fence_mbarrier_init();
+    }
+    __syncthreads();
+    auto issue = [&](int k, int s) {
+        const int yy = ya - L + k;
+        float* dst = sm + s * SLOT;
+        mbar_expect_tx(&full[s], TXB);
+        tma_load_3d(dst, &m.gx, &full[s], c0, yy + gh, x0 - L + gh);
+        tma_load_3d(dst + FS, &m.gy, &full[s], c0, yy + gh, x0 - L + gh);
+    };
+    if (producer) {
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (k < nsteps) issue(k, k);
+    }
+    float2 r2x[T], r2y[T];   // M_x psi_x, M_x psi_y by lead row (step mod T)
+    int slot = 0;
+    unsigned fpar = 0;
+
+#define K2BT_STEP(K, KR, OUT, Y)                                                         \
+    {                                                                                     \
+        const int k_ = (K);                                                               \
+        mbar_wait(&full[slot], fpar);                                                     \
+        const float* buf_ = sm + slot * SLOT + lane;                                      \
+        float2 mx_ = bc2(0.f), my_ = mx_;                                                 \
+        _Pragma("unroll") for (int t = 0; t < T; ++t) {                                   \
+            mx_ = fma2c((float)TP::m(t), ld2(buf_ + t * CC), mx_);                        \
+            my_ = fma2c((float)TP::m(t), ld2(buf_ + FS + t * CC), my_);                   \
+        }                                                                                 \
+        r2x[(KR)] = mx_;                                                                  \
+        r2y[(KR)] = my_;                                                                  \
+        const int cs_ = slot >= L ? slot - L : slot - L + S;                              \
+        if ((OUT) && act && (Y) < yb) {                                                   \
+            float2 mmx = bc2(0.f), mmy = mmx;                                             \
+            _Pragma("unroll") for (int b = 0; b < T; ++b) {                               \
+                mmx = fma2c((float)TP::m(b), r2x[((KR) + 1 + b) % T], mmx);               \
+                mmy = fma2c((float)TP::m(b), r2y[((KR) + 1 + b) % T], mmy);               \
+            }                                                                             \
+            const float* cb = sm + cs_ * SLOT + L * CC + lane;                            \
+            const float2 pxc = ld2(cb), pyc = ld2(cb + FS);                               \
+            const float2 rx = mul2(make_float2(a.alpha_r * mu0, a.alpha_r * mu1),         \
+                                   sub2(mmx, pxc));                                       \
+            const float2 ry = mul2(make_float2(a.alpha_r * nu0, a.alpha_r * nu1),         \
+                                   sub2(mmy, pyc));                                       \
+            const float amu[2] = {fabsf(mu0), fabsf(mu1)}, anu[2] = {fabsf(nu0), fabsf(nu1)}; \
+            const float pxv[2] = {pxc.x, pxc.y}, pyv[2] = {pyc.x, pyc.y};                 \
+            const float rxv[2] = {rx.x, rx.y}, ryv[2] = {ry.x, ry.y};                     \
+            float kx[2], ky[2];                                                           \
+            _Pragma("unroll") for (int h = 0; h < 2; ++h) {                               \
+                kx[h] = k_coef(rxv[h], pxv[h], a.a_abs * a.dx, a.a_sq * a.dx,             \
+                               a.dx * amu[h], amu[h], a.eps);                             \
+                ky[h] = k_coef(ryv[h], pyv[h], a.a_abs * a.dy, a.a_sq * a.dy,             \
+                               a.dy * anu[h], anu[h], a.eps);                             \
+            }                                                                             \
+            const int64_t o = kb0 + (int64_t)(Y) * g.C;                                   \
+            st2(a.kx + o, make_float2(kx[0], kx[1]));                                     \
+            st2(a.ky + o, make_float2(ky[0], ky[1]));                                     \
+        }                                                                                 \
+        if (k_ >= L) {                    /* last read of the centre row's slot */        \
+            __syncwarp();                                                                 \
+            if (tx == 0) mbar_arrive(&empty[cs_]);                                        \
+        }                                                                                 \
+        if (producer && k_ + P < nsteps) {                                                \
+            const int is_ = slot + P >= S ? slot + P - S : slot + P;                      \
+            const int fill_ = (k_ + P) / S;                                               \
+            if (fill_ >= 1) mbar_wait(&empty[is_], (unsigned)((fill_ - 1) & 1));          \
+            issue(k_ + P, is_);                                                           \
+        }                                                                                 \
+        if (++slot == S) { slot = 0; fpar ^= 1u; }                                        \
+    }
+#pragma unroll
+    for (int k = 0; k < 2 * L; ++k) K2BT_STEP(k, k % T, false, 0);
+    int kb = 2 * L;
+    for (int y0 = ya; y0 < yb; y0 += T, kb += T) {
+#pragma unroll
+        for (int s = 0; s < T; ++s) K2BT_STEP(kb + s, (2 * L + s) % T, true, y0 + s);
+    }
+#undef K2BT_STEP
+}
+
+}  // namespace csn

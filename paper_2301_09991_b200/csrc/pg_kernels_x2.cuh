@@ -247,6 +247,18 @@ pg_residual_x2_kernel(const PGResidArgs<float> a) {
     }
 }
 
+// k of one channel (R/discretisation.py:150-158) with explicit rounding, shared by every
+// fp32 diffusivity kernel so their k agree bit for bit:
+//   b = (a_abs d) |R| / (eps + |p|),  s = (a_sq d) R^2 / (eps + |mu| p^2)   (x * rcp_nr),
+//   k = NaN in b or s ? 0 : min(d |mu|, min(b, s))
+__device__ __forceinline__ float k_coef(float R, float p, float cabs, float csq, float cap,
+                                        float amu, float eps) {
+    const float b = __fmul_rn(__fmul_rn(cabs, fabsf(R)), rcp_nr(__fadd_rn(eps, fabsf(p))));
+    const float s = __fmul_rn(__fmul_rn(csq, __fmul_rn(R, R)),
+                              rcp_nr(__fmaf_rn(amu, __fmul_rn(p, p), eps)));
+    return (b != b || s != s) ? 0.f : fminf(cap, fminf(b, s));
+}
+
 // ---------------------------------------------------------------------------------
 // K2 (fp32, L <= 3): iterate averaging fused with the anisotropic diffusivities
 // (R/multigrid.py:217-225, R/discretisation.py:114-161), same two-stage march and
@@ -427,15 +439,10 @@ pg_diffusivity_x2_kernel(const PGKArgs<float> a) {
                     float kx[2], ky[2];
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        // NaN candidate -> 0 (numpy minimum + nan_to_num); dx|mu| is finite
-                        const float bx = fast_div(a.a_abs * a.dx * fabsf(rxv[h]), a.eps + fabsf(pxv[h]));
-                        const float sx = fast_div(a.a_sq * a.dx * (rxv[h] * rxv[h]),
-                                                  a.eps + amu[h] * (pxv[h] * pxv[h]));
-                        const float by = fast_div(a.a_abs * a.dy * fabsf(ryv[h]), a.eps + fabsf(pyv[h]));
-                        const float sy = fast_div(a.a_sq * a.dy * (ryv[h] * ryv[h]),
-                                                  a.eps + anu[h] * (pyv[h] * pyv[h]));
-                        kx[h] = (bx != bx || sx != sx) ? 0.f : fminf(a.dx * amu[h], fminf(bx, sx));
-                        ky[h] = (by != by || sy != sy) ? 0.f : fminf(a.dy * anu[h], fminf(by, sy));
+                        kx[h] = k_coef(rxv[h], pxv[h], a.a_abs * a.dx, a.a_sq * a.dx,
+                                       a.dx * amu[h], amu[h], a.eps);
+                        ky[h] = k_coef(ryv[h], pyv[h], a.a_abs * a.dy, a.a_sq * a.dy,
+                                       a.dy * anu[h], anu[h], a.eps);
                     }
                     const int64_t o = kbase_o + (int64_t)(vo - L) * g.C;
                     st2(a.kx + o, make_float2(kx[0], kx[1]));
@@ -673,15 +680,12 @@ pg_kcoef_x2_kernel(const PGKArgs<float> a, const float* __restrict__ gx_in,
         const float pxv[2] = {pxc.x, pxc.y}, pyv[2] = {pyc.x, pyc.y};                              \
         const float rxv[2] = {rx.x, rx.y}, ryv[2] = {ry.x, ry.y};                                  \
         float kx[2], ky[2];                                                                        \
-        _Pragma("unroll") for (int h = 0; h < 2; ++h) {                                            \
-            const float bx = fast_div(a.a_abs * a.dx * fabsf(rxv[h]), a.eps + fabsf(pxv[h]));      \
-            const float sx = fast_div(a.a_sq * a.dx * (rxv[h] * rxv[h]), a.eps + amu[h] * (pxv[h] * pxv[h])); \
-            const float by = fast_div(a.a_abs * a.dy * fabsf(ryv[h]), a.eps + fabsf(pyv[h]));      \
-            const float sy = fast_div(a.a_sq * a.dy * (ryv[h] * ryv[h]), a.eps + anu[h] * (pyv[h] * pyv[h])); \
-            /* NaN candidate -> 0 (numpy minimum + nan_to_num); dx|mu| is finite */                \
-            kx[h] = (bx != bx || sx != sx) ? 0.f : fminf(a.dx * amu[h], fminf(bx, sx));            \
-            ky[h] = (by != by || sy != sy) ? 0.f : fminf(a.dy * anu[h], fminf(by, sy));            \
-        }                                                                                          \
+        _Pragma("unroll") for (int h = 0; h < 2; ++h) {                                                    \
+            kx[h] = k_coef(rxv[h], pxv[h], a.a_abs * a.dx, a.a_sq * a.dx, a.dx * amu[h],         \
+                           amu[h], a.eps);                                                       \
+            ky[h] = k_coef(ryv[h], pyv[h], a.a_abs * a.dy, a.a_sq * a.dy, a.dy * anu[h],         \
+                           anu[h], a.eps);                                                       \
+        }                                                                                        \
         const int64_t o = kb0 + (int64_t)(Y) * g.C;                                                \
         st2(a.kx + o, make_float2(kx[0], kx[1]));                                                  \
         st2(a.ky + o, make_float2(ky[0], ky[1]));                                                  \

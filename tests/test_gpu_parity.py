@@ -529,3 +529,38 @@ def test_stored_dterm_bitwise(P, tag):
         out.append((s.psi.data.clone(), list(s.history), list(s.pgs.log)))
     assert torch.equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1] and out[0][2] == out[1][2]
+
+
+@pytest.mark.parametrize("nx,ny,na,ng,p", [(32, 24, 8, 1, 3), (20, 18, 4, 2, 2), (16, 13, 2, 1, 1)])
+def test_kcoef_tma_matches_cp_async(P, nx, ny, na, ng, p):
+    """The TMA-staged second diffusivity pass gives the same k, bit for bit, as the
+    cp.async one."""
+    from paper_2301_09991_b200 import _lib
+    from paper_2301_09991_b200.discretisation import diffusivities_into, diffusivities_workspace
+    rng = np.random.default_rng(13)
+    q = P.build_quadrature(na)
+    dx, dy = 1.0 / nx, 1.3 / ny
+    h = 3 * p
+    grid = P.GridSpec(nx, ny, dx, dy, h)
+    fs = P.build_convfem_filters(p, dx, dy)
+    shp = (nx + 2 * h, ny + 2 * h, q.n_dir, ng)
+    psi = torch.as_tensor(rng.standard_normal(shp), dtype=F32, device="cuda")
+    avg0 = torch.as_tensor(rng.standard_normal(shp), dtype=F32, device="cuda")
+    qd = q.device(F32, torch.device("cuda"), dx, dy)
+    gm = _lib.geom(nx, ny, q.n_dir, ng, na, dx, dy)
+    work = diffusivities_workspace(psi, gm, p)
+    out = []
+    for v in (1, 0):
+        prev = _lib.set_tuning("k2_tma", v)
+        try:
+            kx, ky = torch.zeros_like(psi), torch.zeros_like(psi)
+            a_out = torch.zeros_like(psi)
+            diffusivities_into(psi, grid, q.n_dir, ng, na, fs, P.PGConfig(), qd["mu"], qd["nu"],
+                               kx, ky, h, avg_in=avg0.clone(), avg_out=a_out, avg_mode=2,
+                               theta=0.2, gm=gm, work=work)
+            torch.cuda.synchronize()
+            out.append((kx, ky, a_out))
+        finally:
+            _lib.set_tuning("k2_tma", prev)
+    for t1, t0 in zip(out[0], out[1]):
+        assert torch.equal(t1, t0)
