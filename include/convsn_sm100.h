@@ -73,6 +73,9 @@ const char* csn_error_string(int code);
  *                  (mbarrier ring); 0 forces the cp.async kernel (bit-identical);
  *   "k2_tma"     = 1 (default): the fp32 diffusivity path's second pass (k from the
  *                  workspace) stages rows with TMA; 0: cp.async (bit-identical);
+ *   "k2_ws"      = 0 (default): 1 runs the workspace-path diffusivities as one
+ *                  warp-specialised pass (psi_x, psi_y through shared memory;
+ *                  bit-identical; measured slower on C4);
  *   "upwind_tma" = 0 (default): 1 stages the packed smoother's columns with TMA where
  *                  the layout allows (bit-identical; measured 3% slower on C4).
  * The previous value is stored in *prev (nullable). */

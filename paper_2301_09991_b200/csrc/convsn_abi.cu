@@ -26,6 +26,7 @@ int g_tune_sweep_div = 1;
 int g_tune_pg_tma = 1;
 int g_tune_upwind_tma = 0;
 int g_tune_k2_tma = 1;
+int g_tune_k2_ws = 0;   // one-pass K2: 5.0 ms vs 4.2 ms split on C4 (stage 2 starved)
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -275,6 +276,21 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
     constexpr int V = 16 / sizeof(Real);
     const bool vec = vec_ok(g, V);
     if constexpr (sizeof(Real) == 4 && L <= 3) {
+      if (work && g_tune_k2_ws) {   // one pass, warp-specialised (no workspace traffic)
+        const int gx = (int)cdiv(g->nx + 2 * L, WS_TX);
+        const int gy = (int)cdiv((int64_t)g->nd * g->ng, X2_CC);
+        a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T);
+        dim3 grid(gx, gy, (int)cdiv(g->ny + 2 * L, a.ly)), block(32, 2 * WS_TX + 2 * L);
+        if (avg_mode == 2) {
+            if (vec) launch_pg_k_ws<L, true, V>(grid, block, st, a);
+            else launch_pg_k_ws<L, true, 1>(grid, block, st, a);
+        } else {
+            if (vec) launch_pg_k_ws<L, false, V>(grid, block, st, a);
+            else launch_pg_k_ws<L, false, 1>(grid, block, st, a);
+        }
+        CSN_CHECK_LAUNCH();
+        return CSN_OK;
+      }
       if (work) {   // split: K2a gradients -> workspace -> K2b coefficients
         float* gxp = (float*)work;
         float* gyp = gxp + grad_field_elems(g, L);
@@ -497,6 +513,7 @@ int csn_set_tuning(const char* key, int value, int* prev) {
     if (!strcmp(key, "pg_tma")) slot = &g_tune_pg_tma;
     if (!strcmp(key, "upwind_tma")) slot = &g_tune_upwind_tma;
     if (!strcmp(key, "k2_tma")) slot = &g_tune_k2_tma;
+    if (!strcmp(key, "k2_ws")) slot = &g_tune_k2_ws;
     if (!slot) return CSN_E_ARG;
     if (prev) *prev = *slot;
     *slot = value;

@@ -36,6 +36,14 @@ void launch_pg_resid_tma(dim3 grid, dim3 block, cudaStream_t st, const PGResidAr
     pg_residual_tma_kernel<L, MODE, KD><<<grid, block, sm, st>>>(a, maps);
 }
 
+template <int L, bool EMA, int VEC>
+void launch_pg_k_ws(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a) {
+    constexpr size_t sm = pg_k_ws_smem<L, EMA>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_k_ws_kernel<L, EMA, VEC>, sm); attr = true; }
+    pg_k_ws_kernel<L, EMA, VEC><<<grid, block, sm, st>>>(a);
+}
+
 template <int L>
 void launch_pg_kcoef_tma(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a,
                          const KcoefMaps& maps, int gh) {

@@ -20,6 +20,8 @@ void launch_pg_resid_x2(dim3 grid, dim3 block, cudaStream_t st, const PGResidArg
 template <int L, int MODE, int KD>
 void launch_pg_resid_tma(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<float>& a,
                          const PGTmaMaps& maps);
+template <int L, bool EMA, int VEC>
+void launch_pg_k_ws(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a);
 template <int L>
 void launch_pg_kcoef_tma(dim3 grid, dim3 block, cudaStream_t st, const PGKArgs<float>& a,
                          const KcoefMaps& maps, int gh);

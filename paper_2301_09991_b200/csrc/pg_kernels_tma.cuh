@@ -407,3 +407,249 @@ pg_kcoef_tma_kernel(const PGKArgs<float> a, const __grid_constant__ KcoefMaps m,
 }
 
 }  // namespace csn
+
+namespace csn {
+
+// ---------------------------------------------------------------------------------
+// K2 in one pass with warp specialisation: iterate average + psi_x, psi_y (stage 1,
+// the K2a computation) and R, k (stage 2, the K2b computation) in one CTA, psi_x and
+// psi_y handed over through a shared-memory ring instead of an HBM workspace (16 B/DOF
+// of traffic saved).  A CTA owns TX = PG_TX output cells x 64 channels and marches y:
+//   * NW1 = TX + 2l stage-1 warps (one cell each, the output cells +- l): the cp.async
+//     row stager (vacuum rule, EMA on the staged items, owned cells written back), a
+//     named barrier among themselves per row, the x pass and the y ring of K2a; each
+//     psi_x / psi_y row goes to ring slot u mod S2 (0 outside the +-2l band, like the
+//     workspace), then the warp arrives on full2[slot];
+//   * TX stage-2 warps (one output cell each): wait full2, the x pass / y ring / k
+//     formula of K2b, and arrive on empty2 when a row's slot is read for the last time
+//     (as the centre row, l rows later).
+// Stage-1 warps are the old fused kernel's work without its idle edge warps: the two
+// stages run concurrently instead of alternating at a CTA-wide barrier.  Operations
+// and their order are K2a's and K2b's: k and the average are bit-identical to the
+// split path.
+// ---------------------------------------------------------------------------------
+constexpr int WS_TX = PG_TX;      // output cells per CTA
+constexpr int WS_S1 = 4;          // stage-1 input row ring (cp.async)
+
+template <int L>
+struct WsGeom {
+    static constexpr int NW1 = WS_TX + 2 * L;          // stage-1 warps (cells)
+    static constexpr int NW2 = WS_TX;                  // stage-2 warps
+    static constexpr int W1 = WS_TX + 4 * L;           // staged input cells
+    static constexpr int S2 = L + 4;                   // psi_x / psi_y row ring
+    static constexpr int F2 = NW1 * X2_CC;             // floats per psi_x row
+};
+
+template <int L, bool EMA>
+constexpr size_t pg_k_ws_smem() {
+    using G = WsGeom<L>;
+    return ((size_t)WS_S1 * (EMA ? 2 : 1) * G::W1 * X2_CC + (size_t)G::S2 * 2 * G::F2) *
+           sizeof(float);
+}
+
+template <int L, bool EMA, int VEC>
+__global__ void __launch_bounds__(32 * (WS_TX + WS_TX + 2 * L), 1)
+pg_k_ws_kernel(const PGKArgs<float> a) {
+    using TP = UnitTaps<L>;
+    using G = WsGeom<L>;
+    constexpr int T = 2 * L + 1;
+    constexpr int CC = X2_CC;
+    constexpr int NW1 = G::NW1, W1 = G::W1, S2 = G::S2, F2 = G::F2;
+    constexpr int NT1 = 32 * NW1;
+    constexpr int G4 = CC / VEC;
+    constexpr int NI = (W1 * G4 + NT1 - 1) / NT1;
+    constexpr int NF = EMA ? 2 : 1;
+    constexpr int S1 = WS_S1;
+    constexpr int FS = W1 * CC;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    float* s1 = reinterpret_cast<float*>(smraw);               // [S1][NF][W1][CC]
+    float* s2 = s1 + (size_t)S1 * NF * FS;                     // [S2][2][NW1][CC]
+    __shared__ __align__(8) uint64_t full2[S2], empty2[S2];
+
+    const Geo& g = a.g;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int c0 = blockIdx.y * CC;
+    const int c = c0 + 2 * tx;
+    const bool cval = c < g.C;
+    const int cs = cval ? c : g.C - 2;
+    const int x0 = -L + (int)blockIdx.x * WS_TX;              // output band x in [-l, nx+l)
+    const int ya = -L + (int)blockIdx.z * a.ly;               // output band y in [-l, ny+l)
+    const int yb = min(g.ny + L, ya + a.ly);
+    const int nsteps2 = 2 * L + (int)(((yb - ya) + T - 1) / T) * T;   // psi_x rows consumed
+    const int u0 = ya - L;                                    // first psi_x row
+
+    if (ty == 0 && tx == 0) {
+#pragma unroll
+        for (int s = 0; s < S2; ++s) {
+            mbar_init(&full2[s], NW1);
+            mbar_init(&empty2[s], G::NW2);
+        }
+        fence_mbarrier_init();
+    }
+    __syncthreads();
+
+    if (ty < NW1) {
+        // ------------------------------------------------------------- stage 1
+        const int tid = ty * 32 + tx;
+        const int xs1 = x0 - L + ty;                          // this warp's cell
+        const bool inb_x = xs1 >= -2 * L && xs1 < g.nx + 2 * L;
+        const int ox0 = max(x0, 0), ox1 = min(x0 + WS_TX, g.nx);
+        const int oy0 = max(ya, 0), oy1 = min(yb, g.ny);
+        const float2 inv_dx = bc2(a.inv_dx), inv_dy = bc2(a.inv_dy);
+        const float omt = a.omt, theta = a.theta;
+        const bool write_avg = a.avg_mode != 0;
+        // psi_x rows u0 .. u0 + nsteps2 - 1 from lead rows u0 - L ...
+        const int nsteps1 = 2 * L + (int)((nsteps2 + T - 1) / T) * T;
+        FieldDesc fd[2] = {{a.psi, a.psi_h}, {a.avg_in, a.avg_in_h}};
+        Stager<float, VEC, NI, NF, 0, CC> st;
+        st.init(g, fd, x0 - 2 * L, W1, c0, 0, a.mu, a.nu, tid, NT1);
+        const unsigned sbase = (unsigned)__cvta_generic_to_shared(s1);
+        constexpr unsigned FSB = FS * sizeof(float);
+        float* own_ptr[NI];
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int e = tid + i * NT1;
+            const int xi = e / G4, q = e % G4;
+            const int xg = x0 - 2 * L + xi, cc = c0 + q * VEC;
+            own_ptr[i] = (write_avg && e < W1 * G4 && cc < g.C && xg >= ox0 && xg < ox1)
+                             ? a.avg_out + fidx(xg, 0, cc, g.ny, a.avg_out_h, g.C) : nullptr;
+        }
+        const int lane = ty * CC + 2 * tx;
+        float2 rG[T], rM[T];
+#pragma unroll
+        for (int k = 0; k < S1 - 1; ++k) {
+            if (k < nsteps1) st.issue(u0 - L + k, sbase + k * NF * FSB, FSB, a.psi);
+            cp_async_commit();
+        }
+#define WS1_STEP(K, KR, OUT)                                                              \
+        {                                                                                 \
+            const int k_ = (K);                                                           \
+            const int yl_ = u0 - L + k_;                                                  \
+            cp_async_wait<S1 - 2>();                                                      \
+            float* buf_ = s1 + (size_t)(k_ % S1) * NF * FS;                               \
+            if (EMA || write_avg) {                                                       \
+                const bool own_row_ = yl_ >= oy0 && yl_ < oy1;                            \
+                _Pragma("unroll") for (int i = 0; i < NI; ++i) {                          \
+                    const int e = tid + i * NT1;                                          \
+                    if (e < W1 * G4) {                                                    \
+                        float* p_ = buf_ + (e / G4) * CC + (e % G4) * VEC;                \
+                        float pv_[VEC];                                                   \
+                        _Pragma("unroll") for (int vv = 0; vv < VEC; ++vv) {              \
+                            pv_[vv] = p_[vv];                                             \
+                            if (EMA) pv_[vv] = ema_rn(p_[FS + vv], pv_[vv], omt, theta);  \
+                            p_[vv] = pv_[vv];                                             \
+                        }                                                                 \
+                        if (own_ptr[i] && own_row_) {                                     \
+                            float* o_ = own_ptr[i] + (int64_t)yl_ * g.C;                  \
+                            _Pragma("unroll") for (int vv = 0; vv < VEC; ++vv) o_[vv] = pv_[vv]; \
+                        }                                                                 \
+                    }                                                                     \
+                }                                                                         \
+            }                                                                             \
+            asm volatile("bar.sync 1, %0;" ::"r"(NT1) : "memory");                        \
+            {                                                                             \
+                float2 ag_ = bc2(0.f), am_ = ag_;                                         \
+                const float* bp_ = buf_ + lane;                                           \
+                _Pragma("unroll") for (int t = 0; t < T; ++t) {                           \
+                    const float2 p_ = ld2(bp_ + t * CC);                                  \
+                    ag_ = fma2c((float)TP::g(t), p_, ag_);                                \
+                    am_ = fma2c((float)TP::m(t), p_, am_);                                \
+                }                                                                         \
+                rG[(KR)] = ag_;                                                           \
+                rM[(KR)] = am_;                                                           \
+            }                                                                             \
+            const int u_ = yl_ - L;                     /* psi_x row of this step */      \
+            if ((OUT) && u_ - u0 < nsteps2) {                                             \
+                float2 px_ = bc2(0.f), py_ = px_;                                         \
+                _Pragma("unroll") for (int b = 0; b < T; ++b) {                           \
+                    px_ = fma2c((float)TP::m(b), rG[((KR) + 1 + b) % T], px_);            \
+                    py_ = fma2c((float)TP::g(b), rM[((KR) + 1 + b) % T], py_);            \
+                }                                                                         \
+                const bool inb_ = inb_x && cval && u_ >= -2 * L && u_ < g.ny + 2 * L;     \
+                const int n_ = u_ - u0;                                                   \
+                const int sl_ = n_ % S2;                                                  \
+                if (n_ >= S2) mbar_wait(&empty2[sl_], (unsigned)((n_ / S2 - 1) & 1));     \
+                float* w_ = s2 + (size_t)sl_ * 2 * F2 + ty * CC + 2 * tx;                 \
+                st2(w_, inb_ ? mul2(px_, inv_dx) : bc2(0.f));                            \
+                st2(w_ + F2, inb_ ? mul2(py_, inv_dy) : bc2(0.f));                       \
+                __syncwarp();                                                             \
+                if (tx == 0) mbar_arrive(&full2[sl_]);                                    \
+            }                                                                             \
+            if (k_ + S1 - 1 < nsteps1)                                                    \
+                st.issue(u0 - L + k_ + S1 - 1, sbase + ((k_ + S1 - 1) % S1) * NF * FSB, FSB, a.psi); \
+            cp_async_commit();                                                            \
+        }
+#pragma unroll
+        for (int k = 0; k < 2 * L; ++k) WS1_STEP(k, k % T, false);
+        for (int kb = 2 * L; kb < nsteps1; kb += T) {
+#pragma unroll
+            for (int s = 0; s < T; ++s) WS1_STEP(kb + s, (2 * L + s) % T, true);
+        }
+#undef WS1_STEP
+        cp_async_wait<0>();
+    } else {
+        // ------------------------------------------------------------- stage 2
+        const int w2 = ty - NW1;                              // output cell x0 + w2
+        const int x = x0 + w2;
+        const bool act = x < g.nx + L && cval;
+        const int n0 = cs / g.ng, n1 = (cs + 1) / g.ng;
+        const float mu0 = a.mu[n0], mu1 = a.mu[n1], nu0 = a.nu[n0], nu1 = a.nu[n1];
+        const int64_t kb0 = fidx(act ? x : 0, 0, cs, g.ny, a.k_h, g.C);
+        const int lane = w2 * CC + 2 * tx;                    // x pass from stage-1 cell w2
+        float2 r2x[T], r2y[T];
+#define WS2_STEP(K, KR, OUT, Y)                                                           \
+        {                                                                                 \
+            const int k_ = (K);                                                           \
+            const int sl_ = k_ % S2;                                                      \
+            mbar_wait(&full2[sl_], (unsigned)((k_ / S2) & 1));                            \
+            const float* buf_ = s2 + (size_t)sl_ * 2 * F2 + lane;                         \
+            float2 mx_ = bc2(0.f), my_ = mx_;                                             \
+            _Pragma("unroll") for (int t = 0; t < T; ++t) {                               \
+                mx_ = fma2c((float)TP::m(t), ld2(buf_ + t * CC), mx_);                    \
+                my_ = fma2c((float)TP::m(t), ld2(buf_ + F2 + t * CC), my_);               \
+            }                                                                             \
+            r2x[(KR)] = mx_;                                                              \
+            r2y[(KR)] = my_;                                                              \
+            if ((OUT) && act && (Y) < yb) {                                               \
+                float2 mmx = bc2(0.f), mmy = mmx;                                         \
+                _Pragma("unroll") for (int b = 0; b < T; ++b) {                           \
+                    mmx = fma2c((float)TP::m(b), r2x[((KR) + 1 + b) % T], mmx);           \
+                    mmy = fma2c((float)TP::m(b), r2y[((KR) + 1 + b) % T], mmy);           \
+                }                                                                         \
+                const float* cb = s2 + (size_t)((k_ - L) % S2) * 2 * F2 + (w2 + L) * CC + 2 * tx; \
+                const float2 pxc = ld2(cb), pyc = ld2(cb + F2);                           \
+                const float2 rx = mul2(make_float2(a.alpha_r * mu0, a.alpha_r * mu1),     \
+                                       sub2(mmx, pxc));                                   \
+                const float2 ry = mul2(make_float2(a.alpha_r * nu0, a.alpha_r * nu1),     \
+                                       sub2(mmy, pyc));                                   \
+                const float amu[2] = {fabsf(mu0), fabsf(mu1)}, anu[2] = {fabsf(nu0), fabsf(nu1)}; \
+                const float pxv[2] = {pxc.x, pxc.y}, pyv[2] = {pyc.x, pyc.y};             \
+                const float rxv[2] = {rx.x, rx.y}, ryv[2] = {ry.x, ry.y};                 \
+                float kx[2], ky[2];                                                       \
+                _Pragma("unroll") for (int h = 0; h < 2; ++h) {                           \
+                    kx[h] = k_coef(rxv[h], pxv[h], a.a_abs * a.dx, a.a_sq * a.dx,         \
+                                   a.dx * amu[h], amu[h], a.eps);                         \
+                    ky[h] = k_coef(ryv[h], pyv[h], a.a_abs * a.dy, a.a_sq * a.dy,         \
+                                   a.dy * anu[h], anu[h], a.eps);                         \
+                }                                                                         \
+                const int64_t o = kb0 + (int64_t)(Y) * g.C;                               \
+                st2(a.kx + o, make_float2(kx[0], kx[1]));                                 \
+                st2(a.ky + o, make_float2(ky[0], ky[1]));                                 \
+            }                                                                             \
+            if (k_ >= L) {                /* row k_ - L read for the last time (centre) */ \
+                __syncwarp();                                                             \
+                if (tx == 0) mbar_arrive(&empty2[(k_ - L) % S2]);                         \
+            }                                                                             \
+        }
+#pragma unroll
+        for (int k = 0; k < 2 * L; ++k) WS2_STEP(k, k % T, false, 0);
+        int kb = 2 * L;
+        for (int y0 = ya; y0 < yb; y0 += T, kb += T) {
+#pragma unroll
+            for (int s = 0; s < T; ++s) WS2_STEP(kb + s, (2 * L + s) % T, true, y0 + s);
+        }
+#undef WS2_STEP
+    }
+}
+
+}  // namespace csn

@@ -32,6 +32,8 @@ CSN_K32(false, 1) CSN_K32(false, 4) CSN_K32(true, 1) CSN_K32(true, 4)
 template void launch_pg_kcoef_x2<CSN_L, 1>(CSN_ARGS_K(float), const float*, const float*, int);
 template void launch_pg_kcoef_x2<CSN_L, 4>(CSN_ARGS_K(float), const float*, const float*, int);
 template void launch_pg_kcoef_tma<CSN_L>(CSN_ARGS_K(float), const KcoefMaps&, int);
+#define CSN_WS(E, V) template void launch_pg_k_ws<CSN_L, E, V>(CSN_ARGS_K(float));
+CSN_WS(false, 1) CSN_WS(false, 4) CSN_WS(true, 1) CSN_WS(true, 4)
 #else
 #define CSN_K32S(E, V) template void launch_pg_k<float, CSN_L, E, V>(CSN_ARGS_K(float));
 CSN_K32S(false, 1) CSN_K32S(false, 4) CSN_K32S(true, 1) CSN_K32S(true, 4)

@@ -533,8 +533,9 @@ def test_stored_dterm_bitwise(P, tag):
 
 @pytest.mark.parametrize("nx,ny,na,ng,p", [(32, 24, 8, 1, 3), (20, 18, 4, 2, 2), (16, 13, 2, 1, 1)])
 def test_kcoef_tma_matches_cp_async(P, nx, ny, na, ng, p):
-    """The TMA-staged second diffusivity pass gives the same k, bit for bit, as the
-    cp.async one."""
+    """The one-pass warp-specialised diffusivity kernel and the TMA-staged second pass of
+    the split path give the same k and iterate average, bit for bit, as the cp.async
+    split path."""
     from paper_2301_09991_b200 import _lib
     from paper_2301_09991_b200.discretisation import diffusivities_into, diffusivities_workspace
     rng = np.random.default_rng(13)
@@ -550,17 +551,23 @@ def test_kcoef_tma_matches_cp_async(P, nx, ny, na, ng, p):
     gm = _lib.geom(nx, ny, q.n_dir, ng, na, dx, dy)
     work = diffusivities_workspace(psi, gm, p)
     out = []
-    for v in (1, 0):
-        prev = _lib.set_tuning("k2_tma", v)
+    for ws, tma in ((1, 1), (0, 1), (0, 0)):      # one pass / split TMA / split cp.async
+        prev_w = _lib.set_tuning("k2_ws", ws)
+        prev_t = _lib.set_tuning("k2_tma", tma)
         try:
-            kx, ky = torch.zeros_like(psi), torch.zeros_like(psi)
-            a_out = torch.zeros_like(psi)
-            diffusivities_into(psi, grid, q.n_dir, ng, na, fs, P.PGConfig(), qd["mu"], qd["nu"],
-                               kx, ky, h, avg_in=avg0.clone(), avg_out=a_out, avg_mode=2,
-                               theta=0.2, gm=gm, work=work)
-            torch.cuda.synchronize()
-            out.append((kx, ky, a_out))
+            for mode in (1, 2):
+                kx, ky = torch.zeros_like(psi), torch.zeros_like(psi)
+                a_out = torch.zeros_like(psi)
+                diffusivities_into(psi, grid, q.n_dir, ng, na, fs, P.PGConfig(), qd["mu"],
+                                   qd["nu"], kx, ky, h, avg_in=avg0.clone() if mode == 2 else None,
+                                   avg_out=a_out, avg_mode=mode, theta=0.2, gm=gm, work=work)
+                torch.cuda.synchronize()
+                out.append((ws, tma, mode, kx, ky, a_out))
         finally:
-            _lib.set_tuning("k2_tma", prev)
-    for t1, t0 in zip(out[0], out[1]):
-        assert torch.equal(t1, t0)
+            _lib.set_tuning("k2_ws", prev_w)
+            _lib.set_tuning("k2_tma", prev_t)
+    ref = {o[2]: o for o in out if o[0] == 0 and o[1] == 0}
+    for o in out:
+        r = ref[o[2]]
+        for t1, t0 in zip(o[3:], r[3:]):
+            assert torch.equal(t1, t0), o[:3]
