@@ -71,8 +71,8 @@ const char* csn_error_string(int code);
  *                  0: reciprocal product;
  *   "pg_tma"     = 1 (default): fp32 csn_pg_residual stages padded fields with TMA
  *                  (mbarrier ring); 0 forces the cp.async kernel (bit-identical);
- *   "k2_tma"     = 1 (default): the fp32 diffusivity path's second pass (k from the
- *                  workspace) stages rows with TMA; 0: cp.async (bit-identical);
+ *   "k2_tma"     = 0 (default): 1 stages the fp32 diffusivity path's second pass (k
+ *                  from the workspace) with TMA (bit-identical; measured 4% slower);
  *   "k2_ws"      = 0 (default): 1 runs the workspace-path diffusivities as one
  *                  warp-specialised pass (psi_x, psi_y through shared memory;
  *                  bit-identical; measured slower on C4);

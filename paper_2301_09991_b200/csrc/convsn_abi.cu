@@ -25,7 +25,7 @@ int g_tune_upwind_div = 3;
 int g_tune_sweep_div = 1;
 int g_tune_pg_tma = 1;
 int g_tune_upwind_tma = 0;
-int g_tune_k2_tma = 1;
+int g_tune_k2_tma = 0;   // TMA-staged K2b: 2.18 ms vs 2.09 ms cp.async on C4
 int g_tune_k2_ws = 0;   // one-pass K2: 5.0 ms vs 4.2 ms split on C4 (stage 2 starved)
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
