@@ -374,6 +374,7 @@ def run_b200(args, rank, world, local_rank):
                        "order": pd.options["order"], "scheme": pd.options["scheme"],
                        "levels": n_levels, "live_cycles": live,
                        "frozen_cycles": args.steps - live, "cuda_graphs": graphs,
+                       **({"tuning": list(args.tune)} if args.tune else {}),
                        "l2": "per-cycle fields >> 126 MB L2 (no flush needed)"
                        if dof * esz > 4 * 126e6 else "fields partly L2-resident; see DESIGN.md",
                        "parallelism": (f"x-slab domain decomposition over {world} GPUs "
@@ -428,6 +429,8 @@ def main():
                     help="z-mirror fold (half the ordinates, same flux); value counts the "
                          "DOF actually updated, not the full-sphere equivalent")
     ap.add_argument("--graphs", default="auto", choices=["auto", "on", "off"])
+    ap.add_argument("--tune", action="append", default=[], metavar="KEY=VALUE",
+                    help="kernel-variant switch (csn_set_tuning), for A/B timing")
     args = ap.parse_args()
     if args.warmup < 0 or args.steps < 1:
         raise SystemExit("need --steps >= 1")
@@ -442,6 +445,12 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl")
+    if args.tune:
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        from paper_2301_09991_b200 import _lib
+        for kv in args.tune:
+            k, v = kv.split("=")
+            _lib.set_tuning(k, int(v))
     run_b200(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

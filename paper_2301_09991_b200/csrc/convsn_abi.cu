@@ -26,7 +26,8 @@ int g_tune_sweep_div = 1;
 int g_tune_pg_tma = 1;
 int g_tune_upwind_tma = 0;
 int g_tune_k2_tma = 0;   // TMA-staged K2b: 2.18 ms vs 2.09 ms cp.async on C4
-int g_tune_k2_ws = 0;   // one-pass K2: 5.0 ms vs 4.2 ms split on C4 (stage 2 starved)
+int g_tune_k2_ws = 0;
+int g_tune_pg_xb = 0;   // x-blocked residual / sweep (warps per CTA: 4 or 8; 0 = off)   // one-pass K2: 5.0 ms vs 4.2 ms split on C4 (stage 2 starved)
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -173,6 +174,33 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
     const bool vec = vec_ok(g, 16 / (int)sizeof(Real));
     constexpr int V = 16 / sizeof(Real);
     if constexpr (X2) {
+        // x-blocked kernel (two cells per lane), when enabled: any halo, 16-byte staging
+        if constexpr (L <= 3) {
+            if ((g_tune_pg_xb == 4 || g_tune_pg_xb == 8) && vec && dterm_mode == 0) {
+                const int nw = g_tune_pg_xb;
+                const int gxb = (int)cdiv(g->nx, 2 * nw);
+                a.ly = pick_ly((int64_t)gxb * gy, g->ny, T);
+                const int gzb = (int)cdiv(g->ny, a.ly);
+                dim3 gridb(gxb, gy, gzb), blockb(32, nw);
+                if (!out && l1 && !partials) return CSN_E_ARG;
+                const int mode = out ? PG_SWEEP : (a.avg_mode ? PG_RESID_EMA : PG_RESID);
+                if (nw == 4) {
+                    if (mode == PG_SWEEP) launch_pg_resid_xb<L, PG_SWEEP, V, 4>(gridb, blockb, st, a);
+                    else if (mode == PG_RESID_EMA) launch_pg_resid_xb<L, PG_RESID_EMA, V, 4>(gridb, blockb, st, a);
+                    else launch_pg_resid_xb<L, PG_RESID, V, 4>(gridb, blockb, st, a);
+                } else {
+                    if (mode == PG_SWEEP) launch_pg_resid_xb<L, PG_SWEEP, V, 8>(gridb, blockb, st, a);
+                    else if (mode == PG_RESID_EMA) launch_pg_resid_xb<L, PG_RESID_EMA, V, 8>(gridb, blockb, st, a);
+                    else launch_pg_resid_xb<L, PG_RESID, V, 8>(gridb, blockb, st, a);
+                }
+                CSN_CHECK_LAUNCH();
+                if (!out && l1) {
+                    sum_f64_kernel<<<1, 1024, 0, st>>>(partials, (int64_t)gxb * gy * gzb, 1.0, l1);
+                    CSN_CHECK_LAUNCH();
+                }
+                return CSN_OK;
+            }
+        }
         // TMA staging when every staged field is padded (halos read as stored)
         constexpr int W = PG_TX + 2 * L;
         PGTmaMaps maps;
@@ -514,6 +542,7 @@ int csn_set_tuning(const char* key, int value, int* prev) {
     if (!strcmp(key, "upwind_tma")) slot = &g_tune_upwind_tma;
     if (!strcmp(key, "k2_tma")) slot = &g_tune_k2_tma;
     if (!strcmp(key, "k2_ws")) slot = &g_tune_k2_ws;
+    if (!strcmp(key, "pg_xb")) slot = &g_tune_pg_xb;
     if (!slot) return CSN_E_ARG;
     if (prev) *prev = *slot;
     *slot = value;

@@ -3,6 +3,7 @@
 #include "launchers.h"
 #include "pg_kernels_x2.cuh"
 #include "pg_kernels_tma.cuh"
+#include "pg_kernels_xb.cuh"
 
 namespace csn {
 
@@ -25,6 +26,14 @@ void launch_pg_resid_x2(dim3 grid, dim3 block, cudaStream_t st, const PGResidArg
     static bool attr = false;
     if (!attr) { set_smem(pg_residual_x2_kernel<L, MODE, VEC>, sm); attr = true; }
     pg_residual_x2_kernel<L, MODE, VEC><<<grid, block, sm, st>>>(a);
+}
+
+template <int L, int MODE, int VEC, int NW>
+void launch_pg_resid_xb(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<float>& a) {
+    constexpr size_t sm = pg_residual_xb_smem<L, MODE, NW>();
+    static bool attr = false;
+    if (!attr) { set_smem(pg_residual_xb_kernel<L, MODE, VEC, NW>, sm); attr = true; }
+    pg_residual_xb_kernel<L, MODE, VEC, NW><<<grid, block, sm, st>>>(a);
 }
 
 template <int L, int MODE, int KD>

@@ -17,6 +17,8 @@ template <class Real, int L, int MODE, int VEC>
 void launch_pg_resid(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<Real>& a);
 template <int L, int MODE, int VEC>
 void launch_pg_resid_x2(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<float>& a);
+template <int L, int MODE, int VEC, int NW>
+void launch_pg_resid_xb(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<float>& a);
 template <int L, int MODE, int KD>
 void launch_pg_resid_tma(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<float>& a,
                          const PGTmaMaps& maps);

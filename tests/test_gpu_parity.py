@@ -468,6 +468,70 @@ def test_tma_residual_matches_cp_async(P, nx, ny, na, ng, p):
         assert torch.equal(t1, t0), i
 
 
+@pytest.mark.parametrize("nx,ny,na,ng,p", [(32, 24, 8, 1, 3), (20, 18, 4, 2, 2), (17, 13, 2, 1, 1),
+                                           (41, 32, 16, 1, 3), (24, 20, 4, 3, 2)])
+def test_xblocked_residual_matches_x2(P, nx, ny, na, ng, p):
+    """The x-blocked residual / sweep kernel (two cells per lane, 4 or 8 warps per CTA)
+    writes the same r, iterate average and swept psi, bit for bit, as the one-cell
+    packed kernel; the fp64 L1 (summed in another order) agrees to 1e-13."""
+    from paper_2301_09991_b200 import _lib
+    from paper_2301_09991_b200.discretisation import pg_residual_launch
+    rng = np.random.default_rng(6)
+    q = P.build_quadrature(na)
+    dx, dy = 1.0 / nx, 1.3 / ny
+    h, l = 3 * p, p
+    grid = P.GridSpec(nx, ny, dx, dy, h)
+    fs = P.build_convfem_filters(p, dx, dy)
+    shp = (nx + 2 * h, ny + 2 * h, q.n_dir, ng)
+    psi = P.Field(grid, q.n_dir, ng, rng.standard_normal(shp), dtype=F32)
+    kband = np.zeros(shp)
+    kband[h - l:h + nx + l, h - l:h + ny + l] = rng.uniform(0, 0.02, (nx + 2 * l, ny + 2 * l,
+                                                                      q.n_dir, ng))
+    kx = torch.as_tensor(kband, dtype=F32, device="cuda")
+    ky = torch.as_tensor(kband[::-1, ::-1].copy(), dtype=F32, device="cuda")
+    delta = torch.as_tensor(0.1 * rng.standard_normal((nx, ny, q.n_dir, ng)), dtype=F32,
+                            device="cuda")
+    sig = torch.as_tensor(rng.uniform(0.2, 4.0, (nx, ny, ng)), dtype=F32, device="cuda")
+    qt = torch.as_tensor(rng.standard_normal((nx, ny, q.n_dir, ng)), dtype=F32, device="cuda")
+    avg0 = torch.as_tensor(rng.standard_normal(shp), dtype=F32, device="cuda")
+    qd = q.device(F32, torch.device("cuda"), dx, dy)
+    npart = _lib.load().csn_partials_size(_lib.F32, _lib.geom(nx, ny, q.n_dir, ng, na, dx, dy), p)
+    out = {}
+    prev_t = _lib.set_tuning("pg_tma", 0)
+    try:
+        for v in (0, 4, 8):
+            prev = _lib.set_tuning("pg_xb", v)
+            try:
+                res = []
+                for ema in (0, 1, 2):
+                    r = torch.zeros((nx, ny, q.n_dir, ng), dtype=F32, device="cuda")
+                    a = avg0.clone()
+                    parts = torch.zeros(int(npart), dtype=torch.float64, device="cuda")
+                    l1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+                    pg_residual_launch(psi, None, None, q, fs, kx, ky, h, r=r, r_halo=0,
+                                       partials=parts, l1=l1, sigma=sig, qt=qt, per_dof=1,
+                                       consts=qd, avg=a if ema else None, avg_mode=ema,
+                                       theta=0.2)
+                    res += [r, a, l1]
+                sw = torch.zeros_like(psi.data)
+                pg_residual_launch(psi, None, None, q, fs, kx, ky, h, psi_out=sw, out_halo=h,
+                                   delta=delta, delta_halo=0, beta=3.0, sigma=sig, qt=qt,
+                                   per_dof=1, consts=qd)
+                res.append(sw)
+                torch.cuda.synchronize()
+                out[v] = [t.clone() for t in res]
+            finally:
+                _lib.set_tuning("pg_xb", prev)
+    finally:
+        _lib.set_tuning("pg_tma", prev_t)
+    for v in (4, 8):
+        for i, (t1, t0) in enumerate(zip(out[v], out[0])):
+            if t0.dtype == torch.float64:
+                assert abs(float(t1) / float(t0) - 1.0) < 1e-13, (v, i)
+            else:
+                assert torch.equal(t1, t0), (v, i)
+
+
 @pytest.mark.parametrize("nx,ny,na,ng,p", [(32, 24, 8, 1, 3), (20, 18, 4, 2, 2), (16, 13, 2, 1, 1),
                                            (40, 32, 16, 1, 3)])
 def test_split_diffusivities_match_fused(P, nx, ny, na, ng, p):
