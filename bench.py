@@ -240,6 +240,7 @@ def run_b200(args, rank, world, local_rank):
     eng = solver.eng
     graphs = args.graphs == "on" or (args.graphs == "auto" and args.config not in ("c4", "c5w"))
     eng.use_graphs = graphs
+    eng.full_sync = args.full_sync
     dtype = opts.torch_dtype()
     hist = []
     for _ in range(args.warmup):
@@ -278,6 +279,7 @@ def run_b200(args, rank, world, local_rank):
         extra.eng.probe = eng.probe
         for _ in range(min(total, args.warmup + 3)):
             extra.step()
+        torch.cuda.synchronize()
         kernel_timing = ("CUDA events, eager pass of the first W+3 cycles after the timed "
                          "region (the timed region replays CUDA graphs)")
     probe = {k: [a.elapsed_time(b) for a, b in v] for k, v in (eng.probe or {}).items()}
@@ -429,6 +431,8 @@ def main():
                     help="z-mirror fold (half the ordinates, same flux); value counts the "
                          "DOF actually updated, not the full-sphere equivalent")
     ap.add_argument("--graphs", default="auto", choices=["auto", "on", "off"])
+    ap.add_argument("--full-sync", action="store_true",
+                    help="A/B: the host waits for the whole cycle instead of its residual")
     ap.add_argument("--tune", action="append", default=[], metavar="KEY=VALUE",
                     help="kernel-variant switch (csn_set_tuning), for A/B timing")
     args = ap.parse_args()

@@ -428,6 +428,8 @@ class CycleEngine:
         self._seen = set()
         self._cap_stream = None
         self._graph_warm = False
+        self._res_ev = None        # recorded after the residual L1 read-back (cycle part a)
+        self.full_sync = False     # A/B switch: wait for the whole cycle (pre-split behaviour)
         # use_dterm (fp32): the residual stores the k-only coefficient D of psi whenever
         # the diffusivities change and the frozen-cycle residual and the sweep read it
         # (csn_pg_residual dterm_mode; bit-identical).  The sweep then runs in the TMA
@@ -520,29 +522,45 @@ class CycleEngine:
             _lib.call("csn_apply_boundary", _lib.dtype_code(d), self.geoms[0], _lib.ptr(d),
                       g.halo, _lib.ptr(c0["mu"]), _lib.ptr(c0["nu"]), _lib.stream())
 
-        def run():
-            self._launch(plan, g, qt, per_dof, fs, cfg, scheme, n_sweeps)
+        # The cycle is issued in two parts: (a) up to the residual's L1 read-back, (b) the
+        # correction, the sweep and the boundary.  An event between them is all the host
+        # waits for: PGState.observe and the next cycle's plan need only this cycle's
+        # pre-update residual, so the next cycle's launches queue behind (b) while it runs
+        # instead of after an idle device (results unchanged; callers see stream order).
+        if self._res_ev is None:
+            self._res_ev = torch.cuda.Event()
+        run_a = lambda: self._launch_a(plan, g, qt, per_dof, fs, cfg, scheme)
+        run_b = lambda: self._launch_b(plan, g, qt, per_dof, fs, cfg, scheme, n_sweeps)
 
         if self.use_graphs and self.probe is None:
             if not self._graph_warm:      # one-time CUDA-graph machinery cost, off the cycle
                 self._graph_warm = True
                 self._capture(lambda: _lib.call("csn_scale", _lib.F64, _lib.ptr(self.l1), 1, 1.0,
                                                 0, _lib.stream())).replay()
-            graph = self._graphs.get(key)
-            if graph is None and key in self._seen:
-                graph = self._capture(run)
-                self._graphs[key] = graph
-            if graph is not None:
-                graph.replay()
+            graphs = self._graphs.get(key)
+            if graphs is None and key in self._seen:
+                graphs = (self._capture(run_a), self._capture(run_b))
+                self._graphs[key] = graphs
+            if graphs is not None:
+                graphs[0].replay()
+                self._res_ev.record()
+                graphs[1].replay()
             else:
-                run()
+                run_a()
+                self._res_ev.record()
+                run_b()
                 self._seen.add(key)
         else:
-            run()
+            run_a()
+            self._res_ev.record()
+            run_b()
         self._commit(plan, psi, pg_state)
         if not sync:
             return None
-        torch.cuda.current_stream().synchronize()
+        if self.full_sync:
+            torch.cuda.current_stream().synchronize()
+        else:
+            self._res_ev.synchronize()
         res = float(self.res_host[0])
         if self.h.levels[0].quad.folded:    # the mirrored faces carry the same |r|
             res *= 2.0
@@ -636,8 +654,9 @@ class CycleEngine:
                        (None if ema[0] is None else ema[0].data_ptr(),) + ema[1:], plan["pg_sweeps"])
         return plan
 
-    def _launch(self, plan, g, qt, per_dof, fs, cfg, scheme, n_sweeps):
-        """Issue the kernel sequence of a planned cycle on the current stream."""
+    def _launch_a(self, plan, g, qt, per_dof, fs, cfg, scheme):
+        """Issue part (a) of a planned cycle on the current stream: diffusivity refresh,
+        residual (+ fused EMA) and the asynchronous read-back of its L1."""
         L = self.h.levels
         f = L[0]
         c0 = self.consts[0]
@@ -685,6 +704,17 @@ class CycleEngine:
             self._t1("upwind_residual", t)
         self._hook_l1()
         self.res_host.copy_(self.l1, non_blocking=True)
+
+    def _launch_b(self, plan, g, qt, per_dof, fs, cfg, scheme, n_sweeps):
+        """Issue part (b): finest correction, fused PG sweep (or psi -= delta), boundary."""
+        f = self.h.levels[0]
+        c0 = self.consts[0]
+        psi_in = plan["psi"]
+        dt = _lib.dtype_code(psi_in)
+        view = Field.__new__(Field)
+        view.grid = g
+        view.data = psi_in
+        nd, ng = psi_in.shape[2], psi_in.shape[3]
         self.sweep_reach = fs.half_width if scheme == "pg" else 1    # x reach of the update
         pad = self.pad_delta and plan["pg_sweeps"] > 0
         dh = fs.half_width if pad else 0
