@@ -149,17 +149,18 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
         qN = make_float2(q0[ya * qst], q1[ya * qst]);
     }
 
-#define TMA_STEP(K, SK, OUT, Y)                                                       \
+#define TMA_STEP(K, SK, OUT, Y, SLOTC)                                                \
     {                                                                                 \
         const int k_ = (K);                                                           \
+        const int ss_ = (SLOTC) >= 0 ? (SLOTC) : slot;                                \
         float2 sg_ = sgN, q_ = qN, dd_ = dN;                                          \
         if ((OUT) && act && (Y) + 1 < yb) {                                           \
             sgN = make_float2(sig0[((Y) + 1) * g.ng], sig1[((Y) + 1) * g.ng]);       \
             qN = make_float2(q0[((Y) + 1) * qst], q1[((Y) + 1) * qst]);              \
             if (KD == 2) dN = ld2(dt_p + (int64_t)((Y) + 1) * g.C);                  \
         }                                                                             \
-        mbar_wait(&full[slot], fpar);                                                 \
-        const float* buf_ = sm + slot * SLOT;                                         \
+        mbar_wait(&full[ss_], fpar);                                                   \
+        const float* buf_ = sm + ss_ * SLOT;                                           \
         if (EMA && avg_p) {                                                           \
             const int yl_ = ya - L + k_;                                              \
             if (yl_ >= oy0 && yl_ < oy1) {                                            \
@@ -211,7 +212,7 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
                 if (KD != 2) rD[sl_] = fma2c(m_, xd1_, fma2c(s_, xd2_, rD[sl_]));     \
             }                                                                         \
         }                                                                             \
-        const int cs_ = slot >= L ? slot - L : slot - L + S;  /* centre row's slot */ \
+        const int cs_ = ss_ >= L ? ss_ - L : ss_ - L + S;  /* centre row's slot */ \
         if ((OUT) && act && (Y) < yb) {                                               \
             const int y_ = (Y);                                                       \
             const float* cb_ = sm + cs_ * SLOT + L * CC + lane_off;                    \
@@ -240,22 +241,24 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
             if (tx == 0) mbar_arrive(&empty[cs_]);                                    \
         }                                                                             \
         if (producer && k_ + P < nsteps) {                                            \
-            const int is_ = slot + P >= S ? slot + P - S : slot + P;                  \
+            const int is_ = ss_ + P >= S ? ss_ + P - S : ss_ + P;                  \
             const int fill_ = (k_ + P) / S;                                           \
             if (fill_ >= 1) mbar_wait(&empty[is_], (unsigned)((fill_ - 1) & 1));      \
             issue(k_ + P, is_);                                                       \
         }                                                                             \
-        if (++slot == S) { slot = 0; fpar ^= 1u; }                                    \
+        slot = ss_ + 1; if (slot == S) { slot = 0; fpar ^= 1u; }                                 \
     }
 
     // prologue: lead rows ya-L .. ya+L-1 (outputs below ya are never emitted)
 #pragma unroll
-    for (int k = 0; k < 2 * L; ++k) TMA_STEP(k, (k + 1) % T, false, 0);
+    for (int k = 0; k < 2 * L; ++k) TMA_STEP(k, (k + 1) % T, false, 0, k % S);
 
+    // S == T (p = 3): compile-time ring slot per unrolled step (see pg_residual_x2_kernel)
     int kbase = 2 * L;
     for (int y0 = ya; y0 < yb; y0 += T, kbase += T) {
 #pragma unroll
-        for (int s = 0; s < T; ++s) TMA_STEP(kbase + s, s, true, y0 + s);
+        for (int s = 0; s < T; ++s)
+            TMA_STEP(kbase + s, s, true, y0 + s, S == T ? (2 * L + s) % S : -1);
     }
 #undef TMA_STEP
     if (!SWEEP && a.partials) {

@@ -129,16 +129,17 @@ pg_residual_x2_kernel(const PGResidArgs<float> a) {
 
     // One step: stage-ready lead row j = ya - L + K; SK = slot of output row j - L in
     // the pending rings; OUT: output row j - L = Y is complete after this step.
-#define X2_STEP(K, SK, OUT, Y)                                                        \
+#define X2_STEP(K, SK, OUT, Y, SLOTC)                                                 \
     {                                                                                 \
         const int k_ = (K);                                                           \
+        const int ss_ = (SLOTC) >= 0 ? (SLOTC) : slot;                                \
         float2 sg_ = sgN, q_ = qN;                                                    \
         if ((OUT) && act && (Y) + 1 < yb) {                                           \
             sgN = make_float2(sig0[((Y) + 1) * g.ng], sig1[((Y) + 1) * g.ng]);       \
             qN = make_float2(q0[((Y) + 1) * qst], q1[((Y) + 1) * qst]);              \
         }                                                                             \
         cp_async_wait<P - 1>();                                                       \
-        float* buf_ = sm + slot * (NF * FS);                                          \
+        float* buf_ = sm + ss_ * (NF * FS);                                          \
         if (SWEEP) {                                                                  \
             _Pragma("unroll") for (int i = 0; i < NI; ++i) {                          \
                 const int e = tid + i * NT;                                           \
@@ -203,7 +204,7 @@ pg_residual_x2_kernel(const PGResidArgs<float> a) {
         }                                                                             \
         if ((OUT) && act && (Y) < yb) {                                               \
             const int y_ = (Y);                                                       \
-            const int cs_ = slot >= L ? slot - L : slot - L + S;                      \
+            const int cs_ = ss_ >= L ? ss_ - L : ss_ - L + S;                      \
             const float* cb_ = sm + cs_ * (NF * FS) + L * CC + lane_off;              \
             const float2 pc_ = ld2(cb_), kxc_ = ld2(cb_ + FS), kyc_ = ld2(cb_ + 2 * FS); \
             float2 r_ = fma2(hx, mul2(kxc_, rB[SK]), rA[SK]);                         \
@@ -222,21 +223,25 @@ pg_residual_x2_kernel(const PGResidArgs<float> a) {
             }                                                                         \
         }                                                                             \
         if (k_ + P < nsteps) {                                                        \
-            const int is_ = slot + P >= S ? slot + P - S : slot + P;                  \
+            const int is_ = ss_ + P >= S ? ss_ + P - S : ss_ + P;                  \
             st.issue(ya - L + k_ + P, sbase + is_ * SLOTB, FSB, a.psi);               \
         }                                                                             \
         cp_async_commit();                                                            \
-        slot = slot + 1 == S ? 0 : slot + 1;                                          \
+        slot = ss_ + 1 == S ? 0 : ss_ + 1;                                              \
     }
 
     // prologue: lead rows ya-L .. ya+L-1 (outputs below ya are never emitted)
 #pragma unroll
-    for (int k = 0; k < 2 * L; ++k) X2_STEP(k, (k + 1) % T, false, 0);
+    for (int k = 0; k < 2 * L; ++k) X2_STEP(k, (k + 1) % T, false, 0, k % S);
 
+    // when the staging ring is as deep as the tap count (p = 3: S = T = 7) the slot of
+    // every unrolled step is a compile-time constant ((2l + s) mod S): shared addresses
+    // fold into immediates instead of per-step select / multiply chains
     int kbase = 2 * L;
     for (int y0 = ya; y0 < yb; y0 += T, kbase += T) {
 #pragma unroll
-        for (int s = 0; s < T; ++s) X2_STEP(kbase + s, s, true, y0 + s);
+        for (int s = 0; s < T; ++s)
+            X2_STEP(kbase + s, s, true, y0 + s, S == T ? (2 * L + s) % S : -1);
     }
 #undef X2_STEP
     cp_async_wait<0>();
@@ -652,12 +657,13 @@ pg_kcoef_x2_kernel(const PGKArgs<float> a, const float* __restrict__ gx_in,
         cp_async_commit();
     }
     int slot = 0;
-#define K2B_STEP(K, KR, OUT, Y)                                                                    \
+#define K2B_STEP(K, KR, OUT, Y, SLOTC)                                                             \
 {                                                                                                  \
     const int k_ = (K);                                                                            \
+    const int ss_ = (SLOTC) >= 0 ? (SLOTC) : slot;                                                 \
     cp_async_wait<P - 1>();                                                                        \
     __syncthreads();                                                                               \
-    const float* buf_ = sm + slot * (NF * FS) + lane;                                              \
+    const float* buf_ = sm + ss_ * (NF * FS) + lane;                                              \
     float2 mx_ = bc2(0.f), my_ = mx_;                                                              \
     _Pragma("unroll") for (int t = 0; t < T; ++t) {                                                \
         mx_ = fma2c((float)TP::m(t), ld2(buf_ + t * CC), mx_);                                     \
@@ -671,7 +677,7 @@ pg_kcoef_x2_kernel(const PGKArgs<float> a, const float* __restrict__ gx_in,
             mmx = fma2c((float)TP::m(b), r2x[((KR) + 1 + b) % T], mmx);                            \
             mmy = fma2c((float)TP::m(b), r2y[((KR) + 1 + b) % T], mmy);                            \
         }                                                                                          \
-        const int cs_ = slot >= L ? slot - L : slot - L + S;                                       \
+        const int cs_ = ss_ >= L ? ss_ - L : ss_ - L + S;                                       \
         const float* cb = sm + cs_ * (NF * FS) + L * CC + lane;                                    \
         const float2 pxc = ld2(cb), pyc = ld2(cb + FS);                                            \
         const float2 rx = mul2(make_float2(a.alpha_r * mu0, a.alpha_r * mu1), sub2(mmx, pxc));     \
@@ -691,18 +697,19 @@ pg_kcoef_x2_kernel(const PGKArgs<float> a, const float* __restrict__ gx_in,
         st2(a.ky + o, make_float2(ky[0], ky[1]));                                                  \
     }                                                                                              \
     if (k_ + P < nsteps) {                                                                         \
-        const int is_ = slot + P >= S ? slot + P - S : slot + P;                                   \
+        const int is_ = ss_ + P >= S ? ss_ + P - S : ss_ + P;                                   \
         st.issue(ya - L + k_ + P, sbase + is_ * SLOTB, FSB, gx_in);                                \
     }                                                                                              \
     cp_async_commit();                                                                             \
-    slot = slot + 1 == S ? 0 : slot + 1;                                                           \
+    slot = ss_ + 1 == S ? 0 : ss_ + 1;                                                           \
 }
 #pragma unroll
-    for (int k = 0; k < 2 * L; ++k) K2B_STEP(k, k % T, false, 0);
+    for (int k = 0; k < 2 * L; ++k) K2B_STEP(k, k % T, false, 0, k % S);
     int kb = 2 * L;
     for (int y0 = ya; y0 < yb; y0 += T, kb += T) {
 #pragma unroll
-        for (int s = 0; s < T; ++s) K2B_STEP(kb + s, (2 * L + s) % T, true, y0 + s);
+        for (int s = 0; s < T; ++s)
+            K2B_STEP(kb + s, (2 * L + s) % T, true, y0 + s, S == T ? (2 * L + s) % S : -1);
     }
 #undef K2B_STEP
     cp_async_wait<0>();
