@@ -241,6 +241,8 @@ def run_b200(args, rank, world, local_rank):
     graphs = args.graphs == "on" or (args.graphs == "auto" and args.config not in ("c4", "c5w"))
     eng.use_graphs = graphs
     eng.full_sync = args.full_sync
+    if args.pad_delta:             # A/B: sweep through the TMA kernel (padded correction)
+        eng.pad_delta = True
     dtype = opts.torch_dtype()
     hist = []
     for _ in range(args.warmup):
@@ -433,6 +435,8 @@ def main():
     ap.add_argument("--graphs", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--full-sync", action="store_true",
                     help="A/B: the host waits for the whole cycle instead of its residual")
+    ap.add_argument("--pad-delta", action="store_true",
+                    help="A/B: padded finest correction, so the sweep runs in the TMA kernel")
     ap.add_argument("--tune", action="append", default=[], metavar="KEY=VALUE",
                     help="kernel-variant switch (csn_set_tuning), for A/B timing")
     args = ap.parse_args()

@@ -439,7 +439,11 @@ class CycleEngine:
         # K5 -2%, K3E -3%, K3 +5% for the D write, +0.03 ms delta boundary) — the PG
         # kernels are latency-bound at 16 warps/SM, not FMA-bound.
         self.use_dterm = False
-        self.pad_delta = self.use_dterm
+        # pad_delta: the finest correction is written into a buffer padded by l with its
+        # boundary applied, so the fp32 sweep runs in the TMA kernel (psi - delta formed
+        # at each read; C4 sweep 3.56 -> 3.46 ms once the TMA march got compile-time ring
+        # slots, for +0.02 ms of boundary fill on delta)
+        self.pad_delta = self.use_dterm or dtype == torch.float32
         self.delta0p = None
         self.sweep_reach = 1
         self.dterm = None
