@@ -10,14 +10,14 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
     > gpurun_out/rp_ncu_launch.log 2>&1
 A="--steps 1 --warmup 0 --no-e2e --no-cpu"
 cap() {   # tag regex skip
-  ncu --set full --clock-control none --import-source on -k regex:"$2" -s $3 -c 1 \
+  ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"$2" -s $3 -c 1 \
       -o gpurun_out/rp_$1 python bench.py $A > gpurun_out/rp_ncu_$1.log 2>&1
   python tools/ncu_summary.py gpurun_out/rp_$1.ncu-rep 0.0 > gpurun_out/rp_$1_sum.txt 2>&1
-  python tools/sass_hist.py gpurun_out/rp_$1.ncu-rep "$2" 0 > gpurun_out/rp_$1_hist.txt 2>&1
+  python tools/sass_hist.py gpurun_out/rp_$1.ncu-rep "." 0 > gpurun_out/rp_$1_hist.txt 2>&1
   [ "$KEEP" = "$1" ] || rm -f gpurun_out/rp_$1.ncu-rep    # gpurun_out returns <= 64 MiB
 }
-cap k5 "pg_residual_x2" 0 1          # first x2 residual launch of the run = the sweep K5
-cap k3 "pg_residual_tma" 0 1         # first TMA residual launch = K3 (live first cycle)
+cap k5 "pg_residual_tma_kernel<.int.3, .int.2" 0 1   # the fused sweep K5 (TMA kernel, SWEEP mode)
+cap k3 "pg_residual_tma_kernel<.int.3, .int.0" 0 1   # K3 (live first cycle)
 cap k2a "pg_grad_x2" 0 1
 cap k2b "pg_kcoef_x2" 0 1
 cap up "upwind_smooth" 9 1           # finest-level smoother of the first cycle
