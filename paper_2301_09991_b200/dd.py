@@ -53,12 +53,35 @@ class SlabComm:
         rows on each side that has a neighbour from the neighbour's interior edge."""
         raise NotImplementedError
 
+    def exchange_many(self, items):
+        """Ghost exchange of several fields [(t, width, hx)] issued together; returns a
+        handle whose wait() orders the consumer after every transfer (stream-ordered on
+        NCCL: the caller may queue independent work before waiting)."""
+        for t, width, hx in items:
+            self.exchange(t, width, hx)
+        return _Done()
+
     def allreduce_sum_(self, t):
         raise NotImplementedError
 
     def allgather_x(self, t):
         """Concatenate every rank's t along dim 0 (rank order)."""
         raise NotImplementedError
+
+
+class _Done:
+    def wait(self):
+        pass
+
+
+class _Pending:
+    def __init__(self, reqs):
+        self.reqs = reqs
+
+    def wait(self):
+        for r in self.reqs:
+            r.wait()
+        self.reqs = []
 
 
 def _edges(t, width, hx):
@@ -77,9 +100,7 @@ class TorchDistComm(SlabComm):
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
 
-    def exchange(self, t, width, hx):
-        if self.size == 1 or width == 0:
-            return
+    def _ops(self, t, width, hx):
         dist = self.dist
         we, ee, wg, eg = _edges(t, width, hx)
         # x is the slowest axis of a contiguous field: every band is one contiguous block,
@@ -91,8 +112,21 @@ class TorchDistComm(SlabComm):
         if self.rank < self.size - 1:
             ops += [dist.P2POp(dist.isend, ee, self.rank + 1, self.group),
                     dist.P2POp(dist.irecv, eg, self.rank + 1, self.group)]
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+        return ops
+
+    def exchange(self, t, width, hx):
+        self.exchange_many([(t, width, hx)]).wait()
+
+    def exchange_many(self, items):
+        # one grouped launch for every band (point-to-point ops to the same peer are
+        # matched in issue order on both sides)
+        ops = []
+        for t, width, hx in items:
+            if self.size > 1 and width > 0:
+                ops += self._ops(t, width, hx)
+        if not ops:
+            return _Done()
+        return _Pending(self.dist.batch_isend_irecv(ops))
 
     def allreduce_sum_(self, t):
         if self.size > 1:
@@ -232,6 +266,10 @@ class DDCycleEngine(CycleEngine):
         h = self.h.levels[0].grid.halo
         self.comm.exchange(t, width, h)
 
+    def _hook_exchange_many(self, items):
+        h = self.h.levels[0].grid.halo
+        self.comm.exchange_many([(t, w, h) for t, w in items]).wait()
+
     def _hook_l1(self):
         self.comm.allreduce_sum_(self.l1)
 
@@ -241,14 +279,12 @@ class DDCycleEngine(CycleEngine):
         L = self.h.levels
         dt = _lib.dtype_code(r0)
         comm = self.comm
-        # local restriction down the distributed levels; source ghosts for the smoother's
-        # H-column warm-up
-        comm.exchange(self.src_g[0].full, UP_MAX_SWEEPS, GX)
+        # local restriction down the distributed levels (2x2 blocks never straddle ranks,
+        # so it reads no ghosts)
         for i in range(1, len(L)):
             _lib.call("csn_restrict", dt, self.geoms[i - 1], self.geoms[i],
                       _lib.ptr(self.src[i - 1]), 0, _lib.ptr(self.consts[i - 1]["w"]),
                       _lib.ptr(self.consts[i]["w"]), 1, _lib.ptr(self.src[i]), 0, _lib.stream())
-            comm.exchange(self.src_g[i].full, UP_MAX_SWEEPS, GX)
         # gathered coarse hierarchy: restrict the last distributed level onto the coarse
         # level's slab, gather, solve redundantly
         cl = self.coarse_h.levels[0]
@@ -259,7 +295,12 @@ class DDCycleEngine(CycleEngine):
                   _lib.ptr(cl.consts(r0.dtype, r0.device)["w"]), 1, _lib.ptr(local_coarse), 0,
                   _lib.stream())
         full = comm.allgather_x(local_coarse)
+        # every distributed level's source ghosts (the smoother's H-column warm-up) in one
+        # grouped exchange, in flight while the gathered coarse levels are solved
+        src_x = comm.exchange_many([(self.src_g[i].full, UP_MAX_SWEEPS, GX)
+                                    for i in range(len(L))])
         dc = self.coarse_eng.correction(full, n_sweeps, 1.0)
+        src_x.wait()
         w = cl.grid.nx // comm.size
         x0 = comm.rank * w
         ci = self.coarse_init

@@ -496,6 +496,11 @@ class CycleEngine:
     def _hook_exchange(self, name, t, width):
         pass
 
+    def _hook_exchange_many(self, items):
+        """Ghost-row exchange of several padded fields [(tensor, width)] (DD ranks)."""
+        for t, width in items:
+            self._hook_exchange("field", t, width)
+
     def _hook_l1(self):
         pass
 
@@ -676,13 +681,16 @@ class CycleEngine:
             reach = (3 if plan["k2"] is not None else 1) * fs.half_width
         else:
             reach = 1
-        self._hook_exchange("psi", psi_in, reach)
+        avg_x = None
+        if scheme == "pg" and plan["k2"] is not None and plan["k2"][0] is not None:
+            avg_x = plan["k2"][0]
+        # psi (and the averaged iterate before a live refresh) ghosts in one exchange
+        self._hook_exchange_many([(psi_in, reach)] + ([(avg_x, reach)] if avg_x is not None
+                                                       else []))
         if scheme == "pg":
             kx, ky = plan["kx"], plan["ky"]
             if plan["k2"] is not None:
                 avg_in, avg_out, mode, theta = plan["k2"]
-                if avg_in is not None:
-                    self._hook_exchange("avg", avg_in, reach)
                 t = self._t0()
                 if self.k_work is None or self.k_work[0] != (fs.order, psi_in.dtype):
                     self.k_work = ((fs.order, psi_in.dtype),

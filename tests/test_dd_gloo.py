@@ -51,6 +51,33 @@ def _worker(rank, size, port, q):
                                                              dtype=torch.float64)))
         else:
             ok &= bool(torch.all(eg == -1.0))
+        # several fields in one grouped exchange (different widths / halos / shapes),
+        # waited on after unrelated work
+        fields = []
+        for k, (n, h, ww) in enumerate(((8, 5, 3), (4, 5, 2), (6, 3, 1))):
+            f = torch.full((n + 2 * h, 3), -1.0, dtype=torch.float64)
+            for x in range(n):
+                f[h + x] = 1000.0 * k + 100.0 * rank + x
+            fields.append((f, ww, h, n, k))
+        handle = comm.exchange_many([(f, ww, h) for f, ww, h, _, _ in fields])
+        _ = torch.ones(4).sum()
+        handle.wait()
+        for f, ww, h, n, k in fields:
+            _, _, wg2, eg2 = _edges(f, ww, h)
+            if rank > 0:
+                ok &= bool(torch.all(wg2[:, 0] == torch.tensor(
+                    [1000.0 * k + 100.0 * (rank - 1) + x for x in range(n - ww, n)],
+                    dtype=torch.float64)))
+            else:
+                ok &= bool(torch.all(wg2 == -1.0))
+            if rank < size - 1:
+                ok &= bool(torch.all(eg2[:, 0] == torch.tensor(
+                    [1000.0 * k + 100.0 * (rank + 1) + x for x in range(ww)],
+                    dtype=torch.float64)))
+            else:
+                ok &= bool(torch.all(eg2 == -1.0))
+            # ghost rows beyond the exchanged width stay untouched
+            ok &= bool(torch.all(f[:h - ww] == -1.0)) and bool(torch.all(f[h + n + ww:] == -1.0))
         l1 = torch.tensor([1.5 + rank], dtype=torch.float64)
         comm.allreduce_sum_(l1)
         ok &= abs(float(l1) - sum(1.5 + r for r in range(size))) < 1e-15
