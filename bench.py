@@ -268,7 +268,8 @@ def run_b200(args, rank, world, local_rank):
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1)
     if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms], dtype=torch.float64,
+                         device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
@@ -346,6 +347,11 @@ def run_b200(args, rank, world, local_rank):
                 P.power_iteration(prob, opts, inner_iters=inner)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
+        if world > 1:                    # the job's time: the slowest rank
+            w = torch.tensor([wall], dtype=torch.float64,
+                             device=dev if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(w, op=dist.ReduceOp.MAX)
+            wall = float(w.item())
         ncyc = len(res.residual_history)
         h2d = sum(a.nbytes for a in (mf.sigma_s, mf.source, mf.nu_sigma_f, mf.chi))
         h2d += sum(n * esz for n in setup_levels)
@@ -451,8 +457,13 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # CSN_DIST_BACKEND=gloo: plumbing check of the N > 1 path on fewer GPUs than ranks
+        # (bands staged through the host; never a performance number)
+        backend = os.environ.get("CSN_DIST_BACKEND", "nccl")
+        if backend == "gloo":
+            local_rank %= torch.cuda.device_count()
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     if args.tune:
         sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
         from paper_2301_09991_b200 import _lib

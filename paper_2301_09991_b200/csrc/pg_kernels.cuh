@@ -353,7 +353,10 @@ pg_diffusivity_kernel(const PGKArgs<Real> a) {
     const int nsteps = PRE + (int)(((ub + 1 - ua) + T - 1) / T) * T;   // +1: stage-2 lag
     const int64_t kbase_o = fidx(xout ? xs : 0, 0, cs, g.ny, a.k_h, g.C);
 
-    FieldDesc fd[2] = {{a.psi, a.psi_h}, {a.avg_in, a.avg_in_h}};
+    // the staged band is [-3l, nx+3l): the last CTA's overhang past it is never loaded
+    // (past a ghost side it would run off the field)
+    FieldDesc fd[2] = {{a.psi, a.psi_h, -3 * L, g.nx + 3 * L},
+                       {a.avg_in, a.avg_in_h, -3 * L, g.nx + 3 * L}};
     Stager<Real, VEC, NI, NF, 0> st;
     st.init(g, fd, x0s - L, W1, c0, 0, a.mu, a.nu, tid, NT);
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(s1);

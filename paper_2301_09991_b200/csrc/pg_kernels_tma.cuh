@@ -503,7 +503,10 @@ pg_k_ws_kernel(const PGKArgs<float> a) {
         const bool write_avg = a.avg_mode != 0;
         // psi_x rows u0 .. u0 + nsteps2 - 1 from lead rows u0 - L ...
         const int nsteps1 = 2 * L + (int)((nsteps2 + T - 1) / T) * T;
-        FieldDesc fd[2] = {{a.psi, a.psi_h}, {a.avg_in, a.avg_in_h}};
+        // the staged band is [-3l, nx+3l): the last CTA's overhang past it is never loaded
+        // (past a ghost side it would run off the field)
+        FieldDesc fd[2] = {{a.psi, a.psi_h, -3 * L, g.nx + 3 * L},
+                           {a.avg_in, a.avg_in_h, -3 * L, g.nx + 3 * L}};
         Stager<float, VEC, NI, NF, 0, CC> st;
         st.init(g, fd, x0 - 2 * L, W1, c0, 0, a.mu, a.nu, tid, NT1);
         const unsigned sbase = (unsigned)__cvta_generic_to_shared(s1);

@@ -333,7 +333,10 @@ pg_diffusivity_x2_kernel(const PGKArgs<float> a) {
     const int nsteps = PRE + (int)(((ub + 1 - ua) + T - 1) / T) * T;   // +1: stage-2 lag
     const int64_t kbase_o = fidx(xout ? xs : 0, 0, cs, g.ny, a.k_h, g.C);
 
-    FieldDesc fd[2] = {{a.psi, a.psi_h}, {a.avg_in, a.avg_in_h}};
+    // the staged band is [-3l, nx+3l): the last CTA's overhang past it is never loaded
+    // (past a ghost side it would run off the field)
+    FieldDesc fd[2] = {{a.psi, a.psi_h, -3 * L, g.nx + 3 * L},
+                       {a.avg_in, a.avg_in_h, -3 * L, g.nx + 3 * L}};
     Stager<float, VEC, NI, NF, 0, CC> st;
     st.init(g, fd, x0s - L, W1, c0, 0, a.mu, a.nu, tid, NT);
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(s1);
@@ -518,7 +521,10 @@ pg_grad_x2_kernel(const PGKArgs<float> a, float* __restrict__ gx_out,
     const int nsteps = 2 * L + (int)(((yb - ya) + T - 1) / T) * T;
     const int64_t ob = fidx(act ? x : 0, 0, cs, g.ny, gh, g.C);
 
-    FieldDesc fd[2] = {{a.psi, a.psi_h}, {a.avg_in, a.avg_in_h}};
+    // the staged band is [-3l, nx+3l): the last CTA's overhang past it is never loaded
+    // (past a ghost side it would run off the field)
+    FieldDesc fd[2] = {{a.psi, a.psi_h, -3 * L, g.nx + 3 * L},
+                       {a.avg_in, a.avg_in_h, -3 * L, g.nx + 3 * L}};
     Stager<float, VEC, NI, NF, 0, CC> st;
     st.init(g, fd, x0 - L, W, c0, 0, a.mu, a.nu, tid, NT);
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(sm);

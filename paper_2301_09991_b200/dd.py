@@ -75,13 +75,17 @@ class _Done:
 
 
 class _Pending:
-    def __init__(self, reqs):
+    def __init__(self, reqs, copy_back=()):
         self.reqs = reqs
+        self.copy_back = list(copy_back)   # (device ghost band, host receive buffer)
 
     def wait(self):
         for r in self.reqs:
             r.wait()
         self.reqs = []
+        for dst, src in self.copy_back:
+            dst.copy_(src)
+        self.copy_back = []
 
 
 def _edges(t, width, hx):
@@ -99,19 +103,32 @@ class TorchDistComm(SlabComm):
         self.group = group
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
+        # gloo moves host memory only: device bands are staged through the host (the
+        # plumbing check of the N > 1 path on a single GPU; NCCL never takes this path)
+        self.host_staged = dist.get_backend(group) == "gloo"
 
-    def _ops(self, t, width, hx):
+    def _ops(self, t, width, hx, copy_back=None, tag=0):
         dist = self.dist
         we, ee, wg, eg = _edges(t, width, hx)
+        if self.host_staged and t.is_cuda:
+            we, ee = we.cpu(), ee.cpu()
+            hw, he = torch.empty_like(we), torch.empty_like(ee)
+            if self.rank > 0:
+                copy_back.append((wg, hw))
+            if self.rank < self.size - 1:
+                copy_back.append((eg, he))
+            wg, eg = hw, he
         # x is the slowest axis of a contiguous field: every band is one contiguous block,
         # sent from and received into place
         ops = []
+        # tags name the band (item, direction): westward sends match the west
+        # neighbour's eastern receive
         if self.rank > 0:
-            ops += [dist.P2POp(dist.isend, we, self.rank - 1, self.group),
-                    dist.P2POp(dist.irecv, wg, self.rank - 1, self.group)]
+            ops += [dist.P2POp(dist.isend, we, self.rank - 1, self.group, 2 * tag),
+                    dist.P2POp(dist.irecv, wg, self.rank - 1, self.group, 2 * tag + 1)]
         if self.rank < self.size - 1:
-            ops += [dist.P2POp(dist.isend, ee, self.rank + 1, self.group),
-                    dist.P2POp(dist.irecv, eg, self.rank + 1, self.group)]
+            ops += [dist.P2POp(dist.isend, ee, self.rank + 1, self.group, 2 * tag + 1),
+                    dist.P2POp(dist.irecv, eg, self.rank + 1, self.group, 2 * tag)]
         return ops
 
     def exchange(self, t, width, hx):
@@ -120,25 +137,31 @@ class TorchDistComm(SlabComm):
     def exchange_many(self, items):
         # one grouped launch for every band (point-to-point ops to the same peer are
         # matched in issue order on both sides)
-        ops = []
-        for t, width, hx in items:
+        ops, back = [], []
+        for i, (t, width, hx) in enumerate(items):
             if self.size > 1 and width > 0:
-                ops += self._ops(t, width, hx)
+                ops += self._ops(t, width, hx, back, i)
         if not ops:
             return _Done()
-        return _Pending(self.dist.batch_isend_irecv(ops))
+        return _Pending(self.dist.batch_isend_irecv(ops), back)
 
     def allreduce_sum_(self, t):
         if self.size > 1:
-            self.dist.all_reduce(t, group=self.group)
+            if self.host_staged and t.is_cuda:
+                h = t.cpu()
+                self.dist.all_reduce(h, group=self.group)
+                t.copy_(h)
+            else:
+                self.dist.all_reduce(t, group=self.group)
         return t
 
     def allgather_x(self, t):
         if self.size == 1:
             return t
-        parts = [torch.empty_like(t) for _ in range(self.size)]
-        self.dist.all_gather(parts, t.contiguous(), group=self.group)
-        return torch.cat(parts, dim=0)
+        src = t.cpu() if self.host_staged and t.is_cuda else t.contiguous()
+        parts = [torch.empty_like(src) for _ in range(self.size)]
+        self.dist.all_gather(parts, src, group=self.group)
+        return torch.cat(parts, dim=0).to(t.device)
 
 
 class _Hub:

@@ -65,3 +65,52 @@ def test_dd_matches_single_domain(case, size):
         assert r.pg_log == ref.pg_log
         if pd.driver != "fixed_source":
             np.testing.assert_allclose(r.history, ref.history, rtol=1e-12)
+
+
+@pytest.mark.parametrize("case,nx,n_a,size", [("c4", 128, 8, 2), ("c4", 256, 8, 4),
+                                              ("c3", 128, 8, 2), ("c2", 128, 8, 2)])
+def test_dd_fp32_wide_channels(case, nx, n_a, size):
+    """fp32 kernels (packed x2 / TMA / split K2) under x-slab ghosts with >= 256 channels:
+    the last CTA's x overhang past a ghost side must not be loaded (it once faulted)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_2301_09991_b200 as P
+    from paper_2301_09991_b200 import benchmarks as B
+    from paper_2301_09991_b200.problems import problem_from_data
+    pd = {"c4": lambda: B.c4(nx=nx, blocks=4, n_a=n_a, cycles=6),
+          "c2": lambda: B.c2(nx=nx, blocks=8, n_a=n_a, cycles=6),
+          "c3": lambda: B.c3(n_pins=4, cells_per_pin=nx // 4, n_a=n_a, outers=2, inner=3)}[case]()
+    opts = _opts(P, pd, "float32")
+    prob = problem_from_data(pd)
+    ref = P.solve_fixed_source(prob, opts) if pd.driver == "fixed_source" else \
+        P.power_iteration(prob, opts, pd.inner_iters)
+    res = _run_dd(pd, opts, size)
+    for r in res:
+        assert rel_l2(r.phi, ref.phi) < 1e-6
+        np.testing.assert_allclose(r.residual_history, ref.residual_history, rtol=1e-6)
+        assert r.pg_log == ref.pg_log
+
+
+def test_dd_multiprocess_torchrun():
+    """The N > 1 bench path as the driver launches it (torchrun, one process per rank,
+    TorchDistComm), ranks sharing the one GPU over gloo (bands staged through the host):
+    fp32 C4 and C3 at P = 2 reproduce the single-domain solve."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import os
+    import random
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CSN_DIST_BACKEND="gloo")
+    for args in (["c4", "64", "2", "4", "6"], ["c3", "64", "4", "4", "3"]):
+        out = subprocess.run(
+            [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+             "--master-addr", "127.0.0.1", "--master-port", str(29700 + random.randrange(200)),
+             os.path.join(root, "tools", "dd_torchrun_check.py")] + args,
+            env=env, capture_output=True, text=True, timeout=600)
+        line = [l for l in out.stdout.splitlines() if "phi rel-L2" in l]
+        assert out.returncode == 0 and line, out.stdout[-2000:] + out.stderr[-2000:]
+        f = line[-1].split()
+        assert float(f[f.index("rel-L2") + 1]) < 1e-6 and float(f[f.index("max") + 1]) < 1e-6
+        assert line[-1].endswith("log_eq True")
