@@ -279,11 +279,33 @@ class DDCycleEngine(CycleEngine):
         self.use_graphs = False      # host barriers / NCCL calls between launches
         cl = coarse_h.levels[0]
         self.coarse_eng = coarse_h.engine(n_group, dtype, device)
+        # The gathered coarse solve and the local restriction chain are many short,
+        # launch-bound kernels whose count does not shrink with the rank count: each is
+        # replayed from a CUDA graph (captured on first use per sweep count) over
+        # persistent buffers (one process per rank only: ThreadComm ranks launch from
+        # other threads of the process while a capture would be open).
+        self.coarse_graphs = isinstance(comm, TorchDistComm)
+        self._cgraphs = {}
+        self._local_coarse = None
+        self._coarse_in = None
         self.coarse_init = _XGhost((cl.grid.nx // comm.size, cl.grid.ny, cl.quad.n_dir, n_group),
                                    dtype, device)
         self.coarse_geom = cl.geom(n_group, int(west), int(east))
         cgc = cl.grid
         self.coarse_geom.nx = cgc.nx // comm.size
+
+    def _run_graphed(self, key, run):
+        """run() eagerly on first use (allocations, kernel attributes), then capture it
+        once and replay the graph from the next call on."""
+        if not self.coarse_graphs or torch.cuda.is_current_stream_capturing():
+            run()
+            return
+        g = self._cgraphs.get(key)
+        if g is None:
+            run()
+            self._cgraphs[key] = self._capture(run)
+        else:
+            g.replay()
 
     def _hook_exchange(self, name, t, width):
         h = self.h.levels[0].grid.halo
@@ -302,34 +324,47 @@ class DDCycleEngine(CycleEngine):
         L = self.h.levels
         dt = _lib.dtype_code(r0)
         comm = self.comm
-        # local restriction down the distributed levels (2x2 blocks never straddle ranks,
-        # so it reads no ghosts)
-        for i in range(1, len(L)):
-            _lib.call("csn_restrict", dt, self.geoms[i - 1], self.geoms[i],
-                      _lib.ptr(self.src[i - 1]), 0, _lib.ptr(self.consts[i - 1]["w"]),
-                      _lib.ptr(self.consts[i]["w"]), 1, _lib.ptr(self.src[i]), 0, _lib.stream())
-        # gathered coarse hierarchy: restrict the last distributed level onto the coarse
-        # level's slab, gather, solve redundantly
         cl = self.coarse_h.levels[0]
-        local_coarse = torch.empty((cl.grid.nx // comm.size,) + tuple(self.coarse_eng.shapes[0][1:]),
-                                   dtype=r0.dtype, device=r0.device)
-        _lib.call("csn_restrict", dt, self.geoms[-1], self.coarse_geom, _lib.ptr(self.src[-1]), 0,
-                  _lib.ptr(self.consts[-1]["w"]),
-                  _lib.ptr(cl.consts(r0.dtype, r0.device)["w"]), 1, _lib.ptr(local_coarse), 0,
-                  _lib.stream())
-        full = comm.allgather_x(local_coarse)
+        w = cl.grid.nx // comm.size
+        x0 = comm.rank * w
+        ci = self.coarse_init
+        if self._local_coarse is None or self._local_coarse.dtype != r0.dtype:
+            self._local_coarse = torch.empty((w,) + tuple(self.coarse_eng.shapes[0][1:]),
+                                             dtype=r0.dtype, device=r0.device)
+            self._coarse_in = torch.empty((cl.grid.nx,) + tuple(self.coarse_eng.shapes[0][1:]),
+                                          dtype=r0.dtype, device=r0.device)
+            self._cgraphs = {}
+
+        def restrict_local():
+            # local restriction down the distributed levels (2x2 blocks never straddle
+            # ranks, so it reads no ghosts), then onto the coarse level's slab
+            for i in range(1, len(L)):
+                _lib.call("csn_restrict", dt, self.geoms[i - 1], self.geoms[i],
+                          _lib.ptr(self.src[i - 1]), 0, _lib.ptr(self.consts[i - 1]["w"]),
+                          _lib.ptr(self.consts[i]["w"]), 1, _lib.ptr(self.src[i]), 0,
+                          _lib.stream())
+            _lib.call("csn_restrict", dt, self.geoms[-1], self.coarse_geom,
+                      _lib.ptr(self.src[-1]), 0, _lib.ptr(self.consts[-1]["w"]),
+                      _lib.ptr(cl.consts(r0.dtype, r0.device)["w"]), 1,
+                      _lib.ptr(self._local_coarse), 0, _lib.stream())
+
+        def coarse_solve():
+            # redundant solve of the gathered coarse hierarchy; this rank keeps its slab
+            # of the coarse correction plus GX ghost columns
+            dc = self.coarse_eng.correction(self._coarse_in, n_sweeps, 1.0)
+            ci.full.zero_()
+            lo, hi = max(x0 - GX, 0), min(x0 + w + GX, cl.grid.nx)
+            ci.full[lo - (x0 - GX):hi - (x0 - GX)].copy_(dc[lo:hi])
+
+        self._run_graphed(("restrict", r0.data_ptr()), restrict_local)
+        full = comm.allgather_x(self._local_coarse)
         # every distributed level's source ghosts (the smoother's H-column warm-up) in one
         # grouped exchange, in flight while the gathered coarse levels are solved
         src_x = comm.exchange_many([(self.src_g[i].full, UP_MAX_SWEEPS, GX)
                                     for i in range(len(L))])
-        dc = self.coarse_eng.correction(full, n_sweeps, 1.0)
+        self._coarse_in.copy_(full)
+        self._run_graphed(("coarse", n_sweeps), coarse_solve)
         src_x.wait()
-        w = cl.grid.nx // comm.size
-        x0 = comm.rank * w
-        ci = self.coarse_init
-        ci.full.zero_()
-        lo, hi = max(x0 - GX, 0), min(x0 + w + GX, cl.grid.nx)
-        ci.full[lo - (x0 - GX):hi - (x0 - GX)].copy_(dc[lo:hi])
         prev, gc = ci.view, self.coarse_geom
         for i in range(len(L) - 1, -1, -1):
             scale = finest_scale if i == 0 else 1.0
