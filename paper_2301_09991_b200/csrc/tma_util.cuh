@@ -5,6 +5,13 @@
 
 namespace csn {
 
+// suspend-time hint of the mbarrier wait: a waiting warp sleeps in the barrier unit
+// instead of re-issuing try_wait / branch pairs that take issue slots from the warps
+// doing the stencil arithmetic
+#ifndef CSN_MBAR_SUSPEND_NS
+#define CSN_MBAR_SUSPEND_NS 0x989680
+#endif
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return (unsigned)__cvta_generic_to_shared(p);
 }
@@ -25,10 +32,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
         "{\n"
         ".reg .pred p;\n"
         "MBW_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra MBW_%=;\n"
         "}\n" ::"r"(smem_u32(b)),
-        "r"(parity)
+        "r"(parity), "r"(CSN_MBAR_SUSPEND_NS)
         : "memory");
 }
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
