@@ -63,11 +63,13 @@ class AngularQuadrature:
         cache = self.__dict__.setdefault("_dev", {})
         key = (str(dtype), str(device), dx, dy)
         if key not in cache:
-            up = lambda a: torch.tensor(np.array(a), dtype=dtype, device=device)
-            d = {"mu": up(self.mu), "nu": up(self.nu), "w": up(self.weights)}
+            rows = [self.mu, self.nu, self.weights]
             if dx is not None:
-                strm = np.abs(self.mu) / dx + np.abs(self.nu) / dy
-                d["strm"] = up(strm)
+                rows.append(np.abs(self.mu) / dx + np.abs(self.nu) / dy)
+            # one upload per level (the rows are contiguous views of it)
+            t = torch.tensor(np.stack([np.asarray(r, dtype=np.float64) for r in rows]),
+                             dtype=dtype, device=device)
+            d = dict(zip(("mu", "nu", "w", "strm"), t.unbind(0)))
             cache[key] = d
         return cache[key]
 
@@ -114,7 +116,7 @@ def build_quadrature(n_a):
     k = np.arange(n_a, dtype=float)
     t0, t1 = k / n_a, (k + 1) / n_a          # rows towards the pole
     s0, s1 = k / n_a, (k + 1) / n_a          # columns along the equator edge
-    dirs, wts = [], []
+    dirs = []
     for sx, sy, sz in OCTANT_SIGNS:
         va = np.array([sx, 0.0, 0.0])
         vb = np.array([0.0, sy, 0.0])
@@ -127,12 +129,10 @@ def build_quadrature(n_a):
 
         corners = np.stack([pt(s0, t0), pt(s1, t0), pt(s1, t1), pt(s0, t1)], axis=2)
         corners = corners.reshape(n_a * n_a, 4, 3)
-        corners = corners / np.linalg.norm(corners, axis=2, keepdims=True)
-        area, mom = _patch_area_moment(corners)
-        wts.append(area)
-        dirs.append(mom / area[:, None])
-    weights = np.concatenate(wts)
-    directions = np.concatenate(dirs)
+        dirs.append(corners / np.linalg.norm(corners, axis=2, keepdims=True))
+    # every face's patches in one elementwise pass (face-major order kept)
+    weights, mom = _patch_area_moment(np.concatenate(dirs))
+    directions = mom / weights[:, None]
     weights = weights * (FOUR_PI / weights.sum())
     return AngularQuadrature(n_a=n_a, directions=directions, weights=weights,
                              face_index=np.repeat(np.arange(N_FACES), n_a * n_a))
