@@ -23,6 +23,7 @@ threads of one process on one device — used to verify the decomposition agains
 the single-domain solve on a single GPU).
 """
 
+import os
 import threading
 
 import numpy as np
@@ -283,8 +284,13 @@ class DDCycleEngine(CycleEngine):
         # launch-bound kernels whose count does not shrink with the rank count: each is
         # replayed from a CUDA graph (captured on first use per sweep count) over
         # persistent buffers (one process per rank only: ThreadComm ranks launch from
-        # other threads of the process while a capture would be open).
-        self.coarse_graphs = isinstance(comm, TorchDistComm)
+        # other threads of the process while a capture would be open).  Opt-in
+        # (CSN_DD_GRAPHS=1): measured 0.40 -> 0.38 ms of correction per cycle at 8 ranks
+        # (compute only, tools/dd_rank_cost.py) and checked under torchrun + gloo; the
+        # capture runs in thread-local mode beside NCCL's watchdog thread, which no
+        # multi-GPU box has exercised yet.
+        self.coarse_graphs = (isinstance(comm, TorchDistComm)
+                              and os.environ.get("CSN_DD_GRAPHS", "0") == "1")
         self._cgraphs = {}
         self._local_coarse = None
         self._coarse_in = None
@@ -303,7 +309,7 @@ class DDCycleEngine(CycleEngine):
         g = self._cgraphs.get(key)
         if g is None:
             run()
-            self._cgraphs[key] = self._capture(run)
+            self._cgraphs[key] = self._capture(run, "thread_local")
         else:
             g.replay()
 

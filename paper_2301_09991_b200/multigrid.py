@@ -577,7 +577,7 @@ class CycleEngine:
             pg_state.observe(res, cfg.k_freeze_rel)
         return res
 
-    def _capture(self, run):
+    def _capture(self, run, error_mode="global"):
         """Capture `run` into a CUDA graph on a side stream (no GC / cache flush, unlike
         torch.cuda.graph); all buffers are preallocated, nothing allocates inside.  The
         cyclic GC is paused instead: a collection inside the capture could destroy an
@@ -592,7 +592,7 @@ class CycleEngine:
         gc.disable()
         try:
             with torch.cuda.stream(self._cap_stream):
-                graph.capture_begin()
+                graph.capture_begin(capture_error_mode=error_mode)
                 try:
                     run()
                 finally:

@@ -102,8 +102,8 @@ def test_dd_multiprocess_torchrun():
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, CSN_DIST_BACKEND="gloo")
-    for args in (["c4", "64", "2", "4", "6"], ["c3", "64", "4", "4", "3"]):
+    for graphs, args in (("1", ["c4", "64", "2", "4", "6"]), ("0", ["c3", "64", "4", "4", "3"])):
+        env = dict(os.environ, CSN_DIST_BACKEND="gloo", CSN_DD_GRAPHS=graphs)
         out = subprocess.run(
             [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
              "--master-addr", "127.0.0.1", "--master-port", str(29700 + random.randrange(200)),

@@ -39,7 +39,7 @@ opts = P.SolverOptions(**o, pg=P.PGConfig(**(pg or {})), dtype="float32")
 s = Solver(problem_from_data(pd), opts, None) if N == 1 else \
     DDSolver(problem_from_data(pd), opts, None, comm=NullComm(N // 2, N))
 if N > 1:
-    s.eng.coarse_graphs = True      # as under TorchDistComm
+    s.eng.coarse_graphs = os.environ.get("CSN_DD_GRAPHS", "0") == "1"
 for _ in range(W):
     s.step()
 torch.cuda.synchronize()
