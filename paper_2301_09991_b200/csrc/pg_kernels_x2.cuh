@@ -277,7 +277,14 @@ __device__ __forceinline__ float k_coef(float R, float p, float cabs, float csq,
 // composite filters M*G, M*M removes the stage imbalance but reorders the rounding
 // enough to push C2 fp32 past the 1e-5 flux tolerance, so the reference order stays.)
 // ---------------------------------------------------------------------------------
-constexpr int X2_KT = 16;   // stage-1 x cells per CTA
+constexpr int X2_KT = 16;
+
+// resident CTAs per SM the split diffusivity kernels (K2a, K2b) are compiled for:
+// 4 (<= 64 registers) at p = 3 (C4 K2 4.14 -> 4.03 ms), 3 below (C3 p = 1: 0.48 ms at
+// 3, 0.50 ms at 4); tools/ab_k2minb.sh
+#ifndef CSN_K2_MINB
+#define CSN_K2_MINB (L >= 3 ? 4 : 3)
+#endif   // stage-1 x cells per CTA
 
 template <int L, bool EMA>
 constexpr size_t pg_k_x2_smem() {
@@ -485,7 +492,7 @@ constexpr size_t pg_grad_x2_smem() {
 }
 
 template <int L, bool EMA, int VEC>
-__global__ void __launch_bounds__(32 * PG_TX, 3)
+__global__ void __launch_bounds__(32 * PG_TX, CSN_K2_MINB)
 pg_grad_x2_kernel(const PGKArgs<float> a, float* __restrict__ gx_out,
                   float* __restrict__ gy_out, int gh) {
     using TP = UnitTaps<L>;
@@ -614,7 +621,7 @@ constexpr size_t pg_kcoef_x2_smem() {
 }
 
 template <int L, int VEC>
-__global__ void __launch_bounds__(32 * PG_TX, 3)
+__global__ void __launch_bounds__(32 * PG_TX, CSN_K2_MINB)
 pg_kcoef_x2_kernel(const PGKArgs<float> a, const float* __restrict__ gx_in,
                    const float* __restrict__ gy_in, int gh) {
     using TP = UnitTaps<L>;
