@@ -69,17 +69,28 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        self.first = 0
 
     def start(self):
+        """Launch the sampler (before the warm-up: nvidia-smi takes longer to come up
+        than a short timed region lasts) and wait for its first row."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except (OSError, FileNotFoundError):
             self.proc = None
+            return
+        t0 = time.perf_counter()
+        while not self.rows and time.perf_counter() - t0 < 10.0:
+            time.sleep(0.01)
+
+    def mark(self):
+        """The timed region starts: only rows from here on count."""
+        self.first = len(self.rows)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -90,11 +101,15 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t0 = time.perf_counter()     # a region shorter than the period: its next row
+        while len(self.rows) <= self.first and time.perf_counter() - t0 < 0.2:
+            time.sleep(0.005)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
+        self.rows = self.rows[self.first:]
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -245,17 +260,18 @@ def run_b200(args, rank, world, local_rank):
         eng.pad_delta = True
     dtype = opts.torch_dtype()
     hist = []
+    sampler = ClockSampler(local_rank)
+    sampler.start()
     for _ in range(args.warmup):
         hist.append(solver.step())
     # ---- timed region: K cycles, device-timed with CUDA events, clocks sampled
     probe_live = not graphs          # per-kernel events inside the timed region (eager path)
     eng.probe = {} if probe_live else None
     frozen_before = []
-    sampler = ClockSampler(local_rank)
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    sampler.start()
+    sampler.mark()
     n_launch0 = lib.csn_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
