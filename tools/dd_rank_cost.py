@@ -11,6 +11,10 @@ from paper_2301_09991_b200 import benchmarks as B
 from paper_2301_09991_b200.problems import problem_from_data
 from paper_2301_09991_b200.dd import DDSolver, SlabComm, _Done
 from paper_2301_09991_b200.eigen import Solver
+from paper_2301_09991_b200 import _lib
+for kv in filter(None, os.environ.get("CSN_TUNE", "").split(",")):
+    k, v = kv.split("=")
+    _lib.set_tuning(k, int(v))
 
 
 class NullComm(SlabComm):
