@@ -32,6 +32,15 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# The CPU legs (the reference arm and the cpu_baseline subprocess) run the reference's
+# single-threaded NumPy code (R/cli.py:61-62 parses --threads and never uses it): pin
+# every BLAS / OpenMP pool to one thread BEFORE numpy loads, so "1 core" is enforced.
+CPU_THREAD_VARS = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS",
+                   "NUMEXPR_NUM_THREADS", "VECLIB_MAXIMUM_THREADS")
+if "--cpu-sample" in sys.argv or ("--impl" in sys.argv and "reference" in sys.argv):
+    for _v in CPU_THREAD_VARS:
+        os.environ[_v] = "1"
+
 import numpy as np  # noqa: E402
 
 HBM_FALLBACK_GBS = 6650.0
@@ -124,7 +133,10 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- workload
-def workload(name, nx=None):
+def workload(name, nx=None, world=1):
+    """BASELINE config by name; c5w is the weak-scaling C5 variant (512 x 512 cells per
+    rank, stacked along x), c5 the full 1024 x 1024 C5 (strong scaling, >= 4 GPUs: one
+    fp32 field is 60.8 GB)."""
     from paper_2301_09991_b200 import benchmarks as B
     if name == "c1":
         return B.c1()
@@ -135,7 +147,12 @@ def workload(name, nx=None):
     if name == "c4":
         return B.c4() if nx is None else B.c4(nx=nx, blocks=nx // 16)
     if name == "c5w":
-        return B.c5_weak(1)
+        return B.c5_weak(world)
+    if name == "c5":
+        if world < 4:
+            raise SystemExit("c5 (1024^2 x 2048 ordinates x 7 groups, 60.8 GB per fp32 "
+                             "field) needs >= 4 GPUs; use c5w for the per-GPU weak variant")
+        return B.c5()
     raise SystemExit(f"unknown config {name}")
 
 
@@ -164,31 +181,87 @@ def bytes_model(pd, hier, live):
 
 
 # ----------------------------------------------------------------------------- reference arm
-def cpu_sample_problem(name):
-    """Bounded CPU sample of the workload for the oracle (fp64 NumPy, 1 core)."""
+def cpu_sample_problem(name, arm=False):
+    """Bounded CPU sample of the workload for the reference (fp64 NumPy, 1 core).
+
+    c4: the cpu_baseline leg runs one cycle of the 128 x 128, n_a = 8 instance of the
+    C4 generator (~20 s on one core); the reference arm's steps use
+    the 64 x 64, n_a = 8 instance (~2-3 s per cycle, so W + K steps stay within
+    minutes).  Same generator, order, ordinates per face and material statistics."""
     from paper_2301_09991_b200 import benchmarks as B
     if name == "c4":
-        return B.c4(nx=64, blocks=4, n_a=8, cycles=1), "c4 generator at 64x64 cells, n_a=8 (512 ordinates), cubic PG"
+        if arm:
+            return B.c4(nx=64, blocks=4, n_a=8, cycles=1), "c4 generator at 64x64 cells, n_a=8 (512 ordinates), cubic PG"
+        return B.c4(nx=128, blocks=8, n_a=8, cycles=1), "c4 generator at 128x128 cells, n_a=8 (512 ordinates), cubic PG"
     if name == "c2":
         return B.c2(nx=64, blocks=8, n_a=8, cycles=1), "c2 generator at 64x64 cells, n_a=8, quadratic PG"
     if name == "c1":
         return B.c1(cycles=1), "c1 full size"
     if name == "c3":
         return B.c3(n_pins=4, cells_per_pin=16, n_a=8, outers=1, inner=1), "c3 generator 64x64 cells, n_a=8, 2 groups"
+    if name in ("c5", "c5w"):
+        return B.c5(n_pins=4, cells_per_pin=16, n_a=4, outers=1, inner=1), "c5 generator 64x64 cells, n_a=4, 7 groups"
     return B.c4(nx=64, blocks=4, n_a=8, cycles=1), "c4 generator at 64x64 cells, n_a=8"
 
 
-def time_oracle_cycles(pd, steps, warmup):
-    """Run warmup + steps sawtooth cycles of the oracle; return per-cycle wall times."""
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    import oracle as O
+def reference_package():
+    """The unmodified reference `convsn`: the driver's offline install under
+    baseline/_ref, else the read-only source tree (this container only).  None when
+    neither exists (the oracle port stands in)."""
+    for path in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(path, "convsn")):
+            if path not in sys.path:
+                sys.path.insert(0, path)
+            import convsn
+            return convsn, path
+    return None, None
+
+
+def time_reference_cycles(pd, steps, warmup):
+    """warmup + steps multigrid iterations of the reference's own driver loop
+    (`convsn.eigen._run_cycles`, R/eigen.py:138-156: flux, group source,
+    sawtooth_cycle with PGState), one cycle per step; returns (per-cycle seconds,
+    kind, where).  Falls back to the oracle port (oracle/) when `convsn` is absent."""
+    convsn, where = reference_package()
+    times = []
+    if convsn is not None:
+        from convsn import eigen as re
+        from convsn import discretisation as rd
+        from convsn.grid import Field
+        from convsn.materials import CrossSections
+        from convsn.multigrid import PGState
+        from convsn.problems import ProblemSpec
+        mats = [CrossSections(m.name, m.sigma_a, m.sigma_s, m.nu_sigma_f, m.sigma_f, m.chi)
+                for m in pd.materials]
+        prob = ProblemSpec(name=pd.name, nx=pd.nx, ny=pd.ny, dx=pd.dx, dy=pd.dy,
+                           region_map=pd.region_map, materials=mats, source=pd.source,
+                           n_groups=pd.n_groups)
+        o = dict(pd.options)
+        pg = o.pop("pg", None)
+        if pg is not None:
+            o["pg"] = rd.PGConfig(**pg)
+        opts = re.SolverOptions(**o)
+        st = re.setup_transport(prob, opts)
+        psi = Field(st.grid, st.quad.n_dir, st.mat.n_groups)
+        if st.mat.fissile:            # power iteration's start: psi = 1, production 1
+            psi.data[...] = 1.0
+        pgs = PGState(opts.k_avg_theta)
+        fq = None
+        if st.mat.fissile:
+            phi = re.scalar_flux(psi, st.quad)
+            fq = (st.mat.chi * np.einsum("xyg,xyg->xy", st.mat.nu_sigma_f, phi)[:, :, None])[:, :, None, :]
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            psi, _ = re._run_cycles(psi, st, 1, fission_frozen=fq, pg_state=pgs)
+            if i >= warmup:
+                times.append(time.perf_counter() - t0)
+        return times, "reference", f"convsn {getattr(convsn, '__version__', '')} from {where}".strip()
+    import oracle as O      # the port: test infrastructure, the baseline's stand-in only
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from _util import oracle_options, oracle_problem
     st = O.setup(oracle_problem(pd), oracle_options(pd))
-    ng = pd.n_groups
-    data = O.padded(pd.nx, pd.ny, st.h, st.quad.n_dir, ng)
+    data = O.padded(pd.nx, pd.ny, st.h, st.quad.n_dir, pd.n_groups)
     pgs = O.PGState(st.o.k_avg_theta)
-    times = []
     for i in range(warmup + steps):
         t0 = time.perf_counter()
         phi = O.scalar_flux(data, st.h, st.quad.weights)
@@ -197,15 +270,41 @@ def time_oracle_cycles(pd, steps, warmup):
                          st.o.jacobi_sweeps, st.o.pg_sweeps, pgs)
         if i >= warmup:
             times.append(time.perf_counter() - t0)
-    return times
+    return times, "port", "oracle/convsn_port.py (reference not installed)"
+
+
+def threads_used():
+    return max(int(os.environ.get(v, "0") or 0) for v in CPU_THREAD_VARS) or os.cpu_count()
+
+
+def run_cpu_sample(config):
+    """The cpu_baseline leg (a subprocess of the B200 arm, thread pools pinned before
+    numpy loaded): one cycle of the bounded sample; prints one JSON object."""
+    pd, desc = cpu_sample_problem(config)
+    ts, kind, where = time_reference_cycles(pd, 1, 0)
+    print(json.dumps({"value": pd.dof() / ts[0], "unit": "DOF-updates/s",
+                      "cores": threads_used(), "kind": kind,
+                      "sample": f"{desc}; 1 cycle, {ts[0]:.1f} s; {where}; {cpu_model()}, "
+                                f"{threads_used()} thread(s) of {os.cpu_count()} "
+                                f"(single-threaded NumPy)"}), flush=True)
+
+
+def cpu_baseline_subprocess(config):
+    env = dict(os.environ, **{v: "1" for v in CPU_THREAD_VARS})
+    try:
+        out = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-sample", config],
+                             env=env, capture_output=True, text=True, timeout=600)
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except (subprocess.SubprocessError, ValueError, IndexError) as e:
+        return {"value": None, "error": f"cpu baseline failed: {e}"}
 
 
 def run_reference(args, rank):
     if rank != 0:
         return
-    pd, desc = cpu_sample_problem(args.config)
+    pd, desc = cpu_sample_problem(args.config, arm=True)
     steps, warmup = args.steps, args.warmup
-    times = time_oracle_cycles(pd, steps, warmup)
+    times, kind, where = time_reference_cycles(pd, steps, warmup)
     dof = pd.dof()
     total = float(sum(times))
     value = dof * len(times) / total
@@ -215,9 +314,11 @@ def run_reference(args, rank):
         "warmup": warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
         "config": {"workload": f"{args.config} (CPU sample: {desc})", "dof_per_step": dof},
-        "cpu_baseline": {"value": value, "unit": "DOF-updates/s", "cores": 1, "kind": "port",
-                         "sample": desc + f"; {steps} cycles after {warmup} warm-up; "
-                                          f"{cpu_model()}, 1 of {os.cpu_count()} cores"},
+        "cpu_baseline": {"value": value, "unit": "DOF-updates/s", "cores": threads_used(),
+                         "kind": kind,
+                         "sample": desc + f"; {steps} cycles after {warmup} warm-up; {where}; "
+                                          f"{cpu_model()}, {threads_used()} thread(s) of "
+                                          f"{os.cpu_count()} (single-threaded NumPy)"},
         "e2e": {"value": value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -238,7 +339,7 @@ def run_b200(args, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
-    pd = workload(args.config, args.nx)
+    pd = workload(args.config, args.nx, world)
     total = args.warmup + args.steps
     eigen = pd.driver == "power_iteration"
     inner = pd.inner_iters or 1
@@ -253,8 +354,12 @@ def run_b200(args, rank, world, local_rank):
         make = lambda: Solver(prob, opts, inner if eigen else None)
     solver = make()
     eng = solver.eng
-    graphs = args.graphs == "on" or (args.graphs == "auto" and args.config not in ("c4", "c5w"))
-    eng.use_graphs = graphs
+    # whole-cycle CUDA graphs on one GPU only: a DD cycle has NCCL calls and host waits
+    # between its launches (DDCycleEngine keeps its own opt-in coarse-solve graphs)
+    graphs = world == 1 and (args.graphs == "on" or (args.graphs == "auto"
+                                                     and args.config not in ("c4", "c5w")))
+    if world == 1:
+        eng.use_graphs = graphs
     eng.full_sync = args.full_sync
     if args.pad_delta:             # A/B: sweep through the TMA kernel (padded correction)
         eng.pad_delta = True
@@ -380,17 +485,14 @@ def run_b200(args, rank, world, local_rank):
     # ---- CPU baseline (oracle port, bounded sample, rank 0 at N = 1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        spd, desc = cpu_sample_problem(args.config)
-        ts = time_oracle_cycles(spd, 1, 0)
-        cpu = {"value": spd.dof() / ts[0], "unit": "DOF-updates/s", "cores": 1, "kind": "port",
-               "sample": f"{desc}; 1 cycle; {cpu_model()}, 1 of {os.cpu_count()} cores"}
+        cpu = cpu_baseline_subprocess(args.config)
 
     if rank == 0:
         line = {
             "metric": "space-angle DOF-updates/s per sawtooth cycle",
             "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None,
+            "scaling": "weak" if args.config == "c5w" else "strong", "vs_baseline": None,
             "dtype": "f32" if dtype == torch.float32 else "f64",
             "data": "synthetic (seeded BASELINE generators, paper_2301_09991_b200/benchmarks.py)",
             "config": {"workload": f"{args.config}: " + WORKLOADS.get(args.config, ""),
@@ -426,7 +528,10 @@ WORKLOADS = {
     "c2": "1 group, quadratic PG, 128x128 cells, 512 ordinates, 8x8 seeded blocks",
     "c1": "1 group, linear, PG off (alpha_r=0), 64x64, 128 ordinates",
     "c3": "2-group k-eigenvalue, linear PG, 256x256, 512 ordinates, 5 cycles per outer",
-    "c5w": "7-group k-eigenvalue, linear PG, 512x512 per GPU, 2048 ordinates, 3 cycles per outer",
+    "c5w": "7-group k-eigenvalue, linear PG, 512x512 cells per GPU stacked along x "
+           "((512 N) x 512 global), 2048 ordinates, 3 cycles per outer (weak scaling)",
+    "c5": "7-group k-eigenvalue, linear PG, 1024x1024, 2048 ordinates, 64x64 seeded pin "
+          "lattice, 3 cycles per outer (strong scaling, >= 4 GPUs)",
 }
 
 
@@ -461,7 +566,12 @@ def main():
                     help="A/B: padded finest correction, so the sweep runs in the TMA kernel")
     ap.add_argument("--tune", action="append", default=[], metavar="KEY=VALUE",
                     help="kernel-variant switch (csn_set_tuning), for A/B timing")
+    ap.add_argument("--cpu-sample", default=None, metavar="CONFIG",
+                    help="internal: the cpu_baseline leg (one reference cycle, 1 thread)")
     args = ap.parse_args()
+    if args.cpu_sample:
+        run_cpu_sample(args.cpu_sample)
+        return
     if args.warmup < 0 or args.steps < 1:
         raise SystemExit("need --steps >= 1")
     world = int(os.environ.get("WORLD_SIZE", "1"))

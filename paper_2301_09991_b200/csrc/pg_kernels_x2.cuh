@@ -74,8 +74,10 @@ pg_residual_x2_kernel(const PGResidArgs<float> a) {
     const bool act = x < g.nx && cval;
     const int nsteps = 2 * L + (int)(((yb - ya) + T - 1) / T) * T;   // lead rows ya-L ...
 
-    FieldDesc fd[4] = {{a.psi, a.psi_h}, {a.kx, a.k_h}, {a.ky, a.k_h},
-                       {SWEEP ? a.delta : a.avg, SWEEP ? a.delta_h : a.avg_h}};
+    FieldDesc fd[4] = {{a.psi, a.psi_h, -L, g.nx + L}, {a.kx, a.k_h}, {a.ky, a.k_h},
+                       {SWEEP ? a.delta : a.avg, SWEEP ? a.delta_h : a.avg_h, -L, g.nx + L}};
+    // psi / delta staged only on [-l, nx+l): the last CTA's overhang (nx % TX != 0)
+    // is never read by an output and would run past a ghost side's stored rows
     if (EMA) { fd[3].xlo = x0; fd[3].xhi = min(x0 + PG_TX, g.nx); }   // owned columns only
     Stager<float, VEC, NI, NF, 0x6, CC> st;
     st.init(g, fd, x0 - L, W, c0, L, a.mu, a.nu, tid, NT);

@@ -65,8 +65,10 @@ pg_residual_xb_kernel(const PGResidArgs<float> a) {
     const int yb = min(g.ny, ya + a.ly);
     const int nsteps = 2 * L + (int)(((yb - ya) + T - 1) / T) * T;   // lead rows ya-L ...
 
-    FieldDesc fd[4] = {{a.psi, a.psi_h}, {a.kx, a.k_h}, {a.ky, a.k_h},
-                       {SWEEP ? a.delta : a.avg, SWEEP ? a.delta_h : a.avg_h}};
+    FieldDesc fd[4] = {{a.psi, a.psi_h, -L, g.nx + L}, {a.kx, a.k_h}, {a.ky, a.k_h},
+                       {SWEEP ? a.delta : a.avg, SWEEP ? a.delta_h : a.avg_h, -L, g.nx + L}};
+    // psi / delta staged only on [-l, nx+l): the last CTA's overhang (nx % TX != 0)
+    // is never read by an output and would run past a ghost side's stored rows
     if (EMA) { fd[3].xlo = x0; fd[3].xhi = min(x0 + XC, g.nx); }   // owned columns only
     Stager<float, VEC, NI, NF, 0x6, CC> st;
     st.init(g, fd, x0 - L, W, c0, L, a.mu, a.nu, tid, NT);

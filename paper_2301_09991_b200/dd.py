@@ -91,6 +91,10 @@ class _Pending:
 
 def _edges(t, width, hx):
     nx = t.shape[0] - 2 * hx
+    if width > nx or width > hx:
+        # a band wider than the slab would send the sender's own ghost rows
+        raise ValueError(f"halo exchange of width {width} on a slab of {nx} rows "
+                         f"(halo {hx})")
     return (t[hx:hx + width], t[hx + nx - width:hx + nx],       # west / east interior edge
             t[hx - width:hx], t[hx + nx:hx + nx + width])       # west / east ghost rows
 
@@ -404,6 +408,14 @@ class DDSolver(Solver):
         if lg >= nl:
             raise ValueError("hierarchy too shallow to decompose")
         x0, x1 = slab_bounds(gsetup.grid.nx, comm.size, comm.rank)
+        # every exchange must fit in one neighbour's slab: psi ghosts 3l on live cycles,
+        # the smoother's source warm-up (UP_MAX_SWEEPS) and delta's GX columns
+        l = gsetup.filters.half_width if options.scheme == "pg" else 1
+        need = max(3 * l if options.scheme == "pg" else 1, UP_MAX_SWEEPS, GX)
+        if x1 - x0 < need:
+            raise ValueError(f"slab of {x1 - x0} columns per rank is narrower than the "
+                             f"{need}-column halo exchange ({comm.size} ranks, nx = "
+                             f"{gsetup.grid.nx})")
         for l in range(lg + 1):   # every distributed level and the gather level split evenly
             if (gsetup.grid.nx >> l) % comm.size:
                 raise ValueError(f"level {l} extent not divisible by {comm.size} ranks")

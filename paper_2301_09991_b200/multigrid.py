@@ -744,6 +744,8 @@ class CycleEngine:
         if plan["pg_sweeps"] > 0:
             for k in range(plan["pg_sweeps"]):
                 view.data = bufs[k % 2]
+                if k >= 1:      # the previous sweep's output: its ghost rows (DD ranks)
+                    self._hook_exchange_many([(bufs[k % 2], fs.half_width)])
                 t = self._t0()
                 pg_residual_launch(view, None, None, f.quad, fs, plan["kx"], plan["ky"], g.halo,
                                    psi_out=bufs[(k + 1) % 2], out_halo=g.halo,

@@ -91,6 +91,46 @@ def test_dd_fp32_wide_channels(case, nx, n_a, size):
         assert r.pg_log == ref.pg_log
 
 
+@pytest.mark.parametrize("case,dtype,size", [("ragged", "float32", 2), ("sweeps2", "float64", 2),
+                                             ("sweeps2", "float32", 4)])
+def test_dd_ragged_slab_and_pg_sweeps(case, dtype, size):
+    """Slabs whose width is not a multiple of the 8-cell CTA tile (nx = 200 on 2 ranks:
+    the last CTA's overhang must stop at nx + l on a ghost side) and pg_sweeps = 2 (the
+    second sweep reads the first sweep's output, whose ghost rows are exchanged)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_2301_09991_b200 as P
+    from paper_2301_09991_b200 import benchmarks as B
+    from paper_2301_09991_b200.problems import problem_from_data
+    if case == "ragged":
+        pd = B.c4(nx=200, blocks=8, n_a=8, cycles=5)
+    else:
+        pd = B.c2(nx=64, blocks=8, n_a=2 if dtype == "float64" else 8, cycles=6)
+        pd.options["pg_sweeps"] = 2
+    opts = _opts(P, pd, dtype)
+    ref = P.solve_fixed_source(problem_from_data(pd), opts)
+    res = _run_dd(pd, opts, size)
+    tol = 1e-11 if dtype == "float64" else 1e-6
+    for r in res:
+        assert rel_l2(r.phi, ref.phi) < tol
+        np.testing.assert_allclose(r.residual_history, ref.residual_history, rtol=tol)
+        assert r.pg_log == ref.pg_log
+
+
+def test_dd_rejects_narrow_slabs():
+    """A slab narrower than the widest halo exchange (3l psi rows on live cycles) is
+    refused instead of sending the sender's own ghost rows."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_2301_09991_b200 as P
+    from paper_2301_09991_b200 import benchmarks as B
+    from paper_2301_09991_b200.dd import DDSolver, ThreadComm
+    from paper_2301_09991_b200.problems import problem_from_data
+    pd = B.c4(nx=64, blocks=4, n_a=2, cycles=2)
+    with pytest.raises(ValueError, match="narrower"):
+        DDSolver(problem_from_data(pd), _opts(P, pd, "float64"), comm=ThreadComm.make(8)[0])
+
+
 def test_dd_multiprocess_torchrun():
     """The N > 1 bench path as the driver launches it (torchrun, one process per rank,
     TorchDistComm), ranks sharing the one GPU over gloo (bands staged through the host):
