@@ -27,6 +27,20 @@ from .quadrature import coarsen_quadrature
 UP_MAX_SWEEPS = 3   # sweeps per temporally blocked smoother launch (csrc/upwind_kernels.cuh)
 
 
+class _Nvtx:
+    """NVTX range per cycle stage (host-side markers: nsys/ncu --nvtx group the kernels by
+    stage; the C ABI adds one range per entry point).  A no-op without a profiler."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        torch.cuda.nvtx.range_push(self.name)
+
+    def __exit__(self, *a):
+        torch.cuda.nvtx.range_pop()
+
+
 class Level:
     """One level: grid, ordinates, removal (host fp64) and upwind pieces (R/multigrid.py:32-40)."""
 
@@ -524,6 +538,8 @@ class CycleEngine:
         g = psi.grid
         qt, per_dof = source_tensor(q, g.nx, g.ny, psi.n_dir, psi.n_group, d)
         plan = self._plan(psi, fs, cfg, scheme, pg_sweeps, pg_state)
+        nv_cycle = _Nvtx("csn.cycle")
+        nv_cycle.__enter__()
         key = plan["key"] + (qt.data_ptr(), per_dof, n_sweeps, scheme, id(fs), cfg)
 
         if not halo_ok:
@@ -564,6 +580,7 @@ class CycleEngine:
             self._res_ev.record()
             run_b()
         self._commit(plan, psi, pg_state)
+        nv_cycle.__exit__()
         if not sync:
             return None
         if self.full_sync:
@@ -691,6 +708,8 @@ class CycleEngine:
             kx, ky = plan["kx"], plan["ky"]
             if plan["k2"] is not None:
                 avg_in, avg_out, mode, theta = plan["k2"]
+                nv = _Nvtx("csn.k_refresh")
+                nv.__enter__()
                 t = self._t0()
                 if self.k_work is None or self.k_work[0] != (fs.order, psi_in.dtype):
                     self.k_work = ((fs.order, psi_in.dtype),
@@ -699,7 +718,10 @@ class CycleEngine:
                                    g.halo, avg_in=avg_in, avg_out=avg_out, avg_mode=mode,
                                    theta=theta, gm=self.geoms[0], work=self.k_work[1])
                 self._t1("pg_diffusivity", t)
+                nv.__exit__()
             ema = plan["ema"]
+            nv = _Nvtx("csn.residual")
+            nv.__enter__()
             t = self._t0()
             pg_residual_launch(view, None, None, f.quad, fs, kx, ky, g.halo, r=self.r0, r_halo=0,
                                partials=self.partials, l1=self.l1, sigma=self.sigma[0], qt=qt,
@@ -707,6 +729,7 @@ class CycleEngine:
                                theta=ema[2], gm=self.geoms[0], dterm=self.dterm,
                                dterm_mode=plan["kd3"])
             self._t1("pg_residual" if ema[1] == 0 else "pg_residual+ema", t)
+            nv.__exit__()
         else:
             t = self._t0()
             _lib.call("csn_upwind_residual", dt, self.geoms[0], _lib.ptr(psi_in), g.halo,
@@ -733,6 +756,8 @@ class CycleEngine:
         if pad and (self.delta0p is None or self.delta0p.shape[0] != g.nx + 2 * dh):
             self.delta0p = torch.zeros((g.nx + 2 * dh, g.ny + 2 * dh, nd, ng), dtype=psi_in.dtype,
                                        device=psi_in.device)
+        nv = _Nvtx("csn.correction")
+        nv.__enter__()
         t = self._t0()
         delta = self.correction(self.r0, n_sweeps, cfg.beta_diag if scheme == "pg" else 1.0,
                                 self.delta0p if pad else None, dh)
@@ -740,6 +765,9 @@ class CycleEngine:
             _lib.call("csn_apply_boundary", dt, self.geoms[0], _lib.ptr(delta), dh,
                       _lib.ptr(c0["mu"]), _lib.ptr(c0["nu"]), _lib.stream())
         self._t1("correction", t)
+        nv.__exit__()
+        nv = _Nvtx("csn.sweep")
+        nv.__enter__()
         bufs = (plan["psi"], plan["alt"])
         if plan["pg_sweeps"] > 0:
             for k in range(plan["pg_sweeps"]):
@@ -758,6 +786,7 @@ class CycleEngine:
         else:
             _lib.call("csn_sub_interior", dt, self.geoms[0], _lib.ptr(psi_in), g.halo,
                       _lib.ptr(delta), 0, _lib.stream())
+        nv.__exit__()
         t = self._t0()
         _lib.call("csn_apply_boundary", dt, self.geoms[0], _lib.ptr(view.data), g.halo,
                   _lib.ptr(c0["mu"]), _lib.ptr(c0["nu"]), _lib.stream())
