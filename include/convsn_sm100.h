@@ -113,6 +113,18 @@ int csn_upwind_smooth(int dtype, const csn_geom* g, const void* src, int q_per_d
                       int n_sweeps, double diag_scale, void* out, int out_halo,
                       void* stream);
 
+/* The same smoother with its result folded into the iterate instead of stored:
+ * psi[interior] -= delta (R/multigrid.py:335-338 on the finest level fused with
+ * R/multigrid.py:301 `psi.data[interior] -= delta`), psi padded by psi_halo.  The
+ * subtraction is an L2 reduction (fl(psi - delta); REDG.F32 flushes subnormals);
+ * the caller re-applies the boundary to psi's halo afterwards.  psi must not alias
+ * src or init. */
+int csn_upwind_smooth_sub(int dtype, const csn_geom* g, const void* src, int q_per_dof,
+                          int init_mode, const void* init, int init_halo, const csn_geom* gc,
+                          const void* sigma, const void* mu, const void* nu, const void* strm,
+                          int n_sweeps, double diag_scale, void* psi, int psi_halo,
+                          void* stream);
+
 /* R/multigrid.py:110-127,342-353 restrict / restrict_field_array and the
  * normalisation of R/multigrid.py:326 (normalise = 1). w_f, w_c: device
  * quadrature weights [nd] of fine / coarse level (field dtype). */

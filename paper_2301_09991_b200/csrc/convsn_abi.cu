@@ -215,17 +215,23 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
         // TMA staging when every staged field is padded (halos read as stored)
         constexpr int W = PG_TX + 2 * L;
         PGTmaMaps maps;
+        // a sweep without delta (the correction already folded into psi) stages 3 fields
+        const bool fold = out && !delta;
         const bool tma = g_tune_pg_tma && psi_h >= L && k_h >= L &&
-                         (!out || (delta && delta_h >= L)) &&
+                         (!out || fold || (delta && delta_h >= L)) &&
                          field_map(&maps.psi, psi, g, psi_h, W) &&
                          field_map(&maps.kx, kx, g, k_h, W) && field_map(&maps.ky, ky, g, k_h, W) &&
-                         (out ? field_map(&maps.aux, delta, g, delta_h, W)
+                         (out ? (fold || field_map(&maps.aux, delta, g, delta_h, W))
                               : (!a.avg_mode || field_map(&maps.aux, avg, g, avg_h, PG_TX)));
         if (!tma) cudaGetLastError();
         if (dterm_mode && !tma) return CSN_E_SCHEME;      // the stored D needs the TMA kernel
         if (tma) {
             if (!out && l1 && !partials) return CSN_E_ARG;
-            if (out) {
+            if (fold) {
+                if (dterm_mode == 2) launch_pg_resid_tma<L, PG_SWEEPF, 2>(grid, block, st, a, maps);
+                else if (dterm_mode == 0) launch_pg_resid_tma<L, PG_SWEEPF, 0>(grid, block, st, a, maps);
+                else return CSN_E_SCHEME;
+            } else if (out) {
                 if (dterm_mode == 2) launch_pg_resid_tma<L, PG_SWEEP, 2>(grid, block, st, a, maps);
                 else if (dterm_mode == 0) launch_pg_resid_tma<L, PG_SWEEP, 0>(grid, block, st, a, maps);
                 else return CSN_E_SCHEME;
@@ -404,8 +410,9 @@ template <class Real>
 int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int init_mode,
                        const void* init, int init_h, const csn_geom* gc, const void* sigma,
                        const void* mu, const void* nu, const void* strm, int n_sweeps,
-                       double diag_scale, void* out, int out_h, cudaStream_t st) {
+                       double diag_scale, void* out, int out_h, cudaStream_t st, int fold = 0) {
     UpSmoothArgs<Real> a;
+    a.fold = fold;
     a.g = make_geo(*g);
     a.src = (const Real*)src; a.q_per_dof = q_per_dof;
     a.init_mode = init_mode; a.init = (const Real*)init; a.init_h = init_h;
@@ -447,7 +454,7 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
             // (default off: measured on C4 1.18 ms vs 1.15 ms for the register kernel —
             // both sit at ~47% of DRAM bandwidth with 16 warps/SM, so the deeper
             // prefetch does not pay for its shared-memory reads)
-            if (g_tune_upwind_tma && g1 && a.exact_div == 3 && init_mode != 1 && g->na >= 8 &&
+            if (g_tune_upwind_tma && !fold && g1 && a.exact_div == 3 && init_mode != 1 && g->na >= 8 &&
                 g->na <= 32 && g->ny % 4 == 0 && !g->ghost_w && !g->ghost_e &&
                 (init_mode == 0 || (init_h == 0 && a.angle_coarsens))) {
                 UpTmaMaps maps;
@@ -668,6 +675,30 @@ int csn_upwind_smooth(int dtype, const csn_geom* g, const void* src, int q_per_d
     if (init_mode == 1 && init == out && n_sweeps > 0) return CSN_E_ARG;
     return DTYPE_DISPATCH(dtype, upwind_smooth_impl, g, src, q_per_dof, init_mode, init, init_halo,
                           gc, sigma, mu, nu, strm, n_sweeps, diag_scale, out, out_halo, S(stream));
+}
+
+int csn_upwind_smooth_sub(int dtype, const csn_geom* g, const void* src, int q_per_dof,
+                          int init_mode, const void* init, int init_halo, const csn_geom* gc,
+                          const void* sigma, const void* mu, const void* nu, const void* strm,
+                          int n_sweeps, double diag_scale, void* psi, int psi_halo,
+                          void* stream) {
+    CSN_NVTX();
+    if (!geom_ok(g) || !src || !sigma || !mu || !nu || !strm || !psi || n_sweeps < 0 ||
+        n_sweeps > UP_H)
+        return CSN_E_ARG;
+    if (init_mode < 0 || init_mode > 2) return CSN_E_SCHEME;
+    if (init_mode > 0 && !init) return CSN_E_ARG;
+    if (init_mode == 2 && !geom_ok(gc)) return CSN_E_ARG;
+    if (init == psi || src == psi) return CSN_E_ARG;
+    auto run = [&](auto tag) -> int {
+        using Real = decltype(tag);
+        return upwind_smooth_impl<Real>(g, src, q_per_dof, init_mode, init, init_halo, gc, sigma,
+                                        mu, nu, strm, n_sweeps, diag_scale, psi, psi_halo,
+                                        S(stream), 1);
+    };
+    if (dtype == CSN_F32) return run(float());
+    if (dtype == CSN_F64) return run(double());
+    return CSN_E_DTYPE;
 }
 
 int csn_restrict(int dtype, const csn_geom* gf, const csn_geom* gc, const void* fine,

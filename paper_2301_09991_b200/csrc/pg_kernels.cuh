@@ -76,6 +76,10 @@ struct PGResidArgs {
 
 // residual kernel modes: plain residual, residual + fused iterate EMA, fused sweep
 constexpr int PG_RESID = 0, PG_RESID_EMA = 1, PG_SWEEP = 2;
+// PG_SWEEPF (TMA kernel only): the fused sweep on an iterate the finest correction
+// has already folded into (psi' = psi - delta, csn_upwind_smooth_sub): three staged
+// fields, no per-read subtraction
+constexpr int PG_SWEEPF = 3;
 
 template <class Real, int L, int MODE>
 constexpr size_t pg_residual_smem() {

@@ -30,7 +30,10 @@ struct PGTmaMaps {
 
 // ring geometry: a slot holds psi, kx, ky rows (W cells) plus delta (W cells, sweep) or
 // pbar_old (the CTA's PG_TX cells, EMA); PREFETCH rows are in flight ahead of the
-// lead row
+// lead row.  (Measured and not kept: a warp-private shared stash of each warp's centre
+// psi', kx, ky that frees a row's slot right after its lead-row step, so S - 1 rows are
+// in flight instead of S - L - 1 — C4 sweep 3.18 -> 3.33 ms, residual 3.04 -> 3.23 ms:
+// the march does not wait on TMA latency.)
 template <int L, int MODE>
 struct TmaRing {
     static constexpr int FS = (PG_TX + 2 * L) * X2_CC;
@@ -50,19 +53,20 @@ __global__ void __launch_bounds__(32 * PG_TX, L <= 3 ? 2 : 1)
 pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTmaMaps m) {
     // KD 0: D computed here; 1: computed and stored to a.dterm; 2: read from a.dterm
     // (bit-identical: the stored value is the one this kernel would compute)
-    constexpr bool SWEEP = MODE == PG_SWEEP;
+    constexpr bool SWEEP = MODE == PG_SWEEP || MODE == PG_SWEEPF;
+    constexpr bool DSUB = MODE == PG_SWEEP;       // psi' = psi - delta formed per read
     constexpr bool EMA = MODE == PG_RESID_EMA;
     using TP = UnitTaps<L>;
     constexpr int T = 2 * L + 1;
     constexpr int CC = X2_CC;
     constexpr int W = PG_TX + 2 * L;
-    constexpr int NF = MODE == PG_RESID ? 3 : 4;
+    constexpr int NF = (MODE == PG_RESID || MODE == PG_SWEEPF) ? 3 : 4;
     constexpr int S = TmaRing<L, MODE>::S;
     constexpr int P = TmaRing<L, MODE>::PREFETCH;   // (S - L - 1)
     constexpr int FS = W * CC;                     // floats per field row
     constexpr int SLOT = TmaRing<L, MODE>::SLOT;
     constexpr unsigned ROWB = W * CC * sizeof(float);
-    constexpr unsigned TXB = 3 * ROWB + (SWEEP ? ROWB : 0) + (EMA ? PG_TX * CC * sizeof(float) : 0);
+    constexpr unsigned TXB = 3 * ROWB + (DSUB ? ROWB : 0) + (EMA ? PG_TX * CC * sizeof(float) : 0);
     extern __shared__ __align__(128) unsigned char smraw[];
     // 128-byte aligned ring base; pointer arithmetic on smraw keeps the shared address
     // space (a uintptr_t round trip would turn every ring read into a generic LD)
@@ -108,7 +112,7 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
         tma_load_3d(dst, &m.psi, &full[s], c0, yy + a.psi_h, x0 - L + a.psi_h);
         tma_load_3d(dst + FS, &m.kx, &full[s], c0, yy + a.k_h, x0 - L + a.k_h);
         tma_load_3d(dst + 2 * FS, &m.ky, &full[s], c0, yy + a.k_h, x0 - L + a.k_h);
-        if (SWEEP) tma_load_3d(dst + 3 * FS, &m.aux, &full[s], c0, yy + a.delta_h, x0 - L + a.delta_h);
+        if (DSUB) tma_load_3d(dst + 3 * FS, &m.aux, &full[s], c0, yy + a.delta_h, x0 - L + a.delta_h);
         if (EMA) tma_load_3d(dst + 3 * FS, &m.aux, &full[s], c0, yy + a.avg_h, x0 + a.avg_h);
     };
 
@@ -179,7 +183,7 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
             const float* bp_ = buf_ + lane_off;                                       \
             _Pragma("unroll") for (int t_ = 0; t_ < T; ++t_) {                        \
                 float2 p_ = ld2(bp_ + t_ * CC);                                       \
-                if (SWEEP) p_ = sub2(p_, ld2(bp_ + 3 * FS + t_ * CC));                \
+                if (DSUB) p_ = sub2(p_, ld2(bp_ + 3 * FS + t_ * CC));                 \
                 const float2 k1_ = ld2(bp_ + FS + t_ * CC);                          \
                 const float2 k2_ = ld2(bp_ + 2 * FS + t_ * CC);                      \
                 a_g = fma2c((float)TP::g(t_), p_, a_g);                               \
@@ -217,7 +221,7 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
             const int y_ = (Y);                                                       \
             const float* cb_ = sm + cs_ * SLOT + L * CC + lane_off;                    \
             float2 pc_ = ld2(cb_);                                                    \
-            if (SWEEP) pc_ = sub2(pc_, ld2(cb_ + 3 * FS));                            \
+            if (DSUB) pc_ = sub2(pc_, ld2(cb_ + 3 * FS));                             \
             const float2 kxc_ = ld2(cb_ + FS), kyc_ = ld2(cb_ + 2 * FS);             \
             float2 r_ = fma2(hx, mul2(kxc_, rB[SK]), rA[SK]);                         \
             r_ = fma2(hy, mul2(kyc_, rC[SK]), r_);                                    \

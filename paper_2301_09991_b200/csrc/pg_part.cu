@@ -24,6 +24,7 @@ CSN_RES32(0, 1) CSN_RES32(0, 4) CSN_RES32(1, 1) CSN_RES32(1, 4) CSN_RES32(2, 1) 
 #define CSN_TMA(M, KD) \
     template void launch_pg_resid_tma<CSN_L, M, KD>(CSN_ARGS_R(float), const PGTmaMaps&);
 CSN_TMA(0, 0) CSN_TMA(0, 1) CSN_TMA(0, 2) CSN_TMA(1, 0) CSN_TMA(1, 1) CSN_TMA(1, 2) CSN_TMA(2, 0) CSN_TMA(2, 2)
+CSN_TMA(3, 0) CSN_TMA(3, 2)
 #if CSN_L <= 3
 #define CSN_XB(M, NW) template void launch_pg_resid_xb<CSN_L, M, 4, NW>(CSN_ARGS_R(float));
 CSN_XB(0, 4) CSN_XB(1, 4) CSN_XB(2, 4) CSN_XB(0, 8) CSN_XB(1, 8) CSN_XB(2, 8)

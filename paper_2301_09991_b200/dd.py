@@ -271,6 +271,7 @@ class DDCycleEngine(CycleEngine):
         self.x0_levels = x0_levels
         super().__init__(local_h, n_group, dtype, device)
         self.pad_delta = False         # x-ghosted finest correction (see correction)
+        self.fold_delta = False        # the sweep reads delta's exchanged ghost rows
         self.use_dterm = False
         west, east = comm.rank > 0, comm.rank < comm.size - 1
         self.geoms = [lev.geom(n_group, int(west), int(east)) for lev in local_h.levels]

@@ -13,6 +13,7 @@ residual read-back that drives ``PGState``.
 
 import gc
 import itertools
+import os
 import numpy as np
 import torch
 
@@ -193,8 +194,11 @@ def prolong(field, coarse_level, fine_level):
 
 
 def _smooth_chain(level, ng, src, per_dof, init, init_mode, init_halo, gc, n_sweeps, scale,
-                  out, out_halo, spare, sig=None, g=None):
-    """Run n_sweeps upwind sweeps in launches of <= 3 (ping-pong through `spare`)."""
+                  out, out_halo, spare, sig=None, g=None, fold=False):
+    """Run n_sweeps upwind sweeps in launches of <= 3 (ping-pong through `spare`).
+
+    fold: `out` is the iterate and the result is subtracted from its interior
+    (csn_upwind_smooth_sub: the finest correction fused with psi -= delta)."""
     d = out
     c = level.consts(d.dtype, d.device)
     if sig is None:
@@ -202,6 +206,14 @@ def _smooth_chain(level, ng, src, per_dof, init, init_mode, init_halo, gc, n_swe
     if g is None:
         g = level.geom(ng)
     dt = _lib.dtype_code(d)
+    if fold:
+        if n_sweeps > UP_MAX_SWEEPS:
+            raise ValueError("the folded correction runs in one launch (<= 3 sweeps)")
+        _lib.call("csn_upwind_smooth_sub", dt, g, _lib.ptr(src), per_dof, init_mode,
+                  _lib.ptr(init), init_halo, gc, _lib.ptr(sig), _lib.ptr(c["mu"]),
+                  _lib.ptr(c["nu"]), _lib.ptr(c["strm"]), n_sweeps, float(scale), _lib.ptr(out),
+                  out_halo, _lib.stream())
+        return out
     first = min(n_sweeps, UP_MAX_SWEEPS)
     bufs = [out, spare]
     k = 0
@@ -452,13 +464,19 @@ class CycleEngine:
         # removes 23% of the sweep's FMAs but the cycle is unchanged (11.03 vs 11.04 ms:
         # K5 -2%, K3E -3%, K3 +5% for the D write, +0.03 ms delta boundary) — the PG
         # kernels are latency-bound at 16 warps/SM, not FMA-bound.
-        self.use_dterm = False
+        self.use_dterm = os.environ.get("CSN_DTERM", "0") == "1" and dtype == torch.float32
         # pad_delta: the finest correction is written into a buffer padded by l with its
         # boundary applied, so the fp32 sweep runs in the TMA kernel (psi - delta formed
         # at each read; C4 sweep 3.56 -> 3.46 ms once the TMA march got compile-time ring
         # slots, for +0.02 ms of boundary fill on delta)
         self.pad_delta = self.use_dterm or dtype == torch.float32
         self.delta0p = None
+        # fold_delta: the finest smoother subtracts its correction from psi in place
+        # (csn_upwind_smooth_sub, an L2 reduction) and the fused sweep stages psi' alone
+        # (TMA PG_SWEEPF: 3 fields, no per-read psi - delta); same DRAM bytes per cycle,
+        # a quarter fewer shared-memory reads and FP adds in the sweep.  CSN_FOLD=0 turns
+        # it off (A/B); domain decomposition keeps the exchanged delta.
+        self.fold_delta = os.environ.get("CSN_FOLD", "1") != "0"
         self.sweep_reach = 1
         self.dterm = None
         self._dkey = None
@@ -478,9 +496,10 @@ class CycleEngine:
         self.probe.setdefault(name, []).append((ev0, ev))
 
     # ---------------------------------------------------------------- correction
-    def correction(self, r0, n_sweeps, finest_scale, out0=None, out0_halo=0):
+    def correction(self, r0, n_sweeps, finest_scale, out0=None, out0_halo=0, fold=False):
         """Restrict r0 through the hierarchy, smooth upward; returns the finest delta
-        (into out0, a padded buffer with halo out0_halo, when given)."""
+        (into out0, a padded buffer with halo out0_halo, when given; with ``fold`` out0
+        is the iterate and the finest delta is subtracted from it instead)."""
         L = self.h.levels
         dt = _lib.dtype_code(r0)
         src = [r0] + self.src[1:]
@@ -500,7 +519,8 @@ class CycleEngine:
             if i == 0 and out0 is not None:
                 spare = torch.empty_like(out0) if n_sweeps > UP_MAX_SWEEPS else None
                 prev = _smooth_chain(L[0], self.ng, src[0], 1, init, mode, 0, gc, n_sweeps,
-                                     scale, out0, out0_halo, spare, self.sigma[0], self.geoms[0])
+                                     scale, out0, out0_halo, spare, self.sigma[0], self.geoms[0],
+                                     fold)
                 break
             prev = _smooth_chain(L[i], self.ng, src[i], 1, init, mode, 0, gc, n_sweeps, scale,
                                  self.delta[i], 0, self.spare[i], self.sigma[i], self.geoms[i])
@@ -751,7 +771,8 @@ class CycleEngine:
         view.data = psi_in
         nd, ng = psi_in.shape[2], psi_in.shape[3]
         self.sweep_reach = fs.half_width if scheme == "pg" else 1    # x reach of the update
-        pad = self.pad_delta and plan["pg_sweeps"] > 0
+        fold = (self.fold_delta and plan["pg_sweeps"] > 0 and n_sweeps <= UP_MAX_SWEEPS)
+        pad = self.pad_delta and plan["pg_sweeps"] > 0 and not fold
         dh = fs.half_width if pad else 0
         if pad and (self.delta0p is None or self.delta0p.shape[0] != g.nx + 2 * dh):
             self.delta0p = torch.zeros((g.nx + 2 * dh, g.ny + 2 * dh, nd, ng), dtype=psi_in.dtype,
@@ -759,8 +780,15 @@ class CycleEngine:
         nv = _Nvtx("csn.correction")
         nv.__enter__()
         t = self._t0()
-        delta = self.correction(self.r0, n_sweeps, cfg.beta_diag if scheme == "pg" else 1.0,
-                                self.delta0p if pad else None, dh)
+        if fold:
+            # psi' = psi - delta in place, then its boundary (R/multigrid.py:301, :166)
+            self.correction(self.r0, n_sweeps, cfg.beta_diag, psi_in, g.halo, fold=True)
+            _lib.call("csn_apply_boundary", dt, self.geoms[0], _lib.ptr(psi_in), g.halo,
+                      _lib.ptr(c0["mu"]), _lib.ptr(c0["nu"]), _lib.stream())
+            delta = None
+        else:
+            delta = self.correction(self.r0, n_sweeps, cfg.beta_diag if scheme == "pg" else 1.0,
+                                    self.delta0p if pad else None, dh)
         if pad:
             _lib.call("csn_apply_boundary", dt, self.geoms[0], _lib.ptr(delta), dh,
                       _lib.ptr(c0["mu"]), _lib.ptr(c0["nu"]), _lib.stream())
@@ -772,7 +800,12 @@ class CycleEngine:
         if plan["pg_sweeps"] > 0:
             for k in range(plan["pg_sweeps"]):
                 view.data = bufs[k % 2]
-                if k >= 1:      # the previous sweep's output: its ghost rows (DD ranks)
+                if k >= 1:
+                    # the previous sweep's output: boundary (R/multigrid.py:166; the TMA
+                    # sweep reads halos as stored), then its ghost rows on DD ranks (the
+                    # boundary kernel also fills ghost sides; the exchange overwrites them)
+                    _lib.call("csn_apply_boundary", dt, self.geoms[0], _lib.ptr(bufs[k % 2]),
+                              g.halo, _lib.ptr(c0["mu"]), _lib.ptr(c0["nu"]), _lib.stream())
                     self._hook_exchange_many([(bufs[k % 2], fs.half_width)])
                 t = self._t0()
                 pg_residual_launch(view, None, None, f.quad, fs, plan["kx"], plan["ky"], g.halo,

@@ -723,3 +723,28 @@ def test_headline_kernels_pinned(P, tag, dtype):
                                rtol=1e-9 if dtype == "float64" else 1e-4)
     np.testing.assert_array_equal(_log(res), g["pg_log"])
     print(f"PIN {tag} {dtype} phi_rel_l2 {err:.3e} bound {tol:.3e}")
+
+
+@pytest.mark.parametrize("tag,dtype", [("c4_64n8", "float32"), ("c2_reduced", "float32"),
+                                       ("c2_reduced", "float64"), ("c3_reduced", "float32"),
+                                       ("c1_alpha_r", "float32")])
+def test_folded_correction_bitwise(P, tag, dtype):
+    """The finest correction folded into the iterate (csn_upwind_smooth_sub: psi -= delta
+    by L2 reduction, then the 3-field TMA sweep) gives the same solve bit for bit as the
+    stored correction + 4-field sweep (R/multigrid.py:301-304)."""
+    from paper_2301_09991_b200 import benchmarks as B
+    from paper_2301_09991_b200.eigen import Solver
+    from paper_2301_09991_b200.problems import problem_from_data
+    make = PINNED.get(tag) or DRIVERS[tag][0]
+    pd = make(B)
+    o = dict(pd.options)
+    pg = o.pop("pg", None)
+    opts = P.SolverOptions(**o, pg=P.PGConfig(**(pg or {})), dtype=dtype)
+    out = []
+    for fold in (False, True):
+        s = Solver(problem_from_data(pd), opts, pd.inner_iters)
+        s.eng.fold_delta = fold
+        out.append(s.run())
+    np.testing.assert_array_equal(out[0].phi, out[1].phi)
+    np.testing.assert_array_equal(out[0].residual_history, out[1].residual_history)
+    assert out[0].pg_log == out[1].pg_log
