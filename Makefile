@@ -3,7 +3,7 @@
 # so `make -j` compiles them in parallel; the ptxas reports land in build/ptxas.log.
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude --expt-relaxed-constexpr
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude --expt-relaxed-constexpr $(EXTRA)
 PKG := paper_2301_09991_b200
 CSRC := $(PKG)/csrc
 HDR := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/convsn_sm100.h

@@ -164,9 +164,42 @@ def options_for(P, pd, dtype, cycles=None, fold=False):
     return P.SolverOptions(**o, pg=P.PGConfig(**(pg or {})), dtype=dtype, fold_z=fold)
 
 
-def per_dof_bytes(kernel, esz):
-    return {"pg_sweep": 5, "pg_residual": 4, "pg_residual+ema": 6, "pg_diffusivity": 5,
+def per_dof_bytes(kernel, esz, eng=None):
+    """Algorithmic bytes per finest DOF of one launch: the fused sweep reads
+    psi, delta, kx, ky and writes psi (20 B fp32) — or, with the correction folded into
+    the iterate (CycleEngine.fold_delta: the finest smoother already formed psi' = psi -
+    delta), reads psi', kx, ky and writes psi (16 B)."""
+    sweep = getattr(eng, "sweep_elems", 5) if eng is not None else 5
+    return {"pg_sweep": sweep, "pg_residual": 4, "pg_residual+ema": 6, "pg_diffusivity": 5,
             "ema": 3, "upwind_residual": 2}.get(kernel, 0) * esz
+
+
+def fp32_peak_tflops(peaks):
+    """CUDA-core FP32 peak, derived (the driver measures no FP32 figure): 148 SMs x 128
+    FP32 lanes x 2 flops x the measured maximum SM clock."""
+    return 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+
+
+def sweep_roofline(pd, ldof, esz, eng, ms_k, peak, peak_kind, peaks):
+    """Roofline of the fused PG sweep (K5) from its event-timed launch duration: HBM
+    (algorithmic bytes / duration vs the measured copy bandwidth) and FP32 (the
+    reference formulation's 32T + 22 flops per DOF, vs the derived FP32 peak).
+    The bound is whichever roof is lower for this order: bytes/BW vs flops/P."""
+    bpl = per_dof_bytes("pg_sweep", esz, eng) * ldof
+    order = pd.options.get("order", 1)
+    flops = (32 * (2 * order + 1) + 22) * ldof
+    fpk = fp32_peak_tflops(peaks)
+    t_hbm = bpl / (peak * 1e9)
+    t_fp = flops / (fpk * 1e12)
+    hbm = {"achieved": bpl / (ms_k * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+           "frac": t_hbm / (ms_k * 1e-3), "bytes_per_launch": bpl,
+           "bytes_per_dof": bpl / ldof,
+           "peak_source": ("measured (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
+                           else "fallback 6.65 TB/s")}
+    fp = {"achieved": flops / (ms_k * 1e-3) / 1e12, "peak": fpk, "unit": "TFLOP/s",
+          "frac": t_fp / (ms_k * 1e-3), "flops_per_dof": flops / ldof,
+          "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (no measured FP32 peak)"}
+    return hbm, fp, ("fp32" if t_fp > t_hbm else "hbm"), max(t_hbm, t_fp) / (ms_k * 1e-3)
 
 
 def bytes_model(pd, hier, live):
@@ -289,13 +322,20 @@ def run_cpu_sample(config):
                                 f"(single-threaded NumPy)"}), flush=True)
 
 
-def cpu_baseline_subprocess(config):
+def cpu_baseline_start(config):
+    """Start the cpu_baseline leg in a subprocess (1 thread, its own core) so it runs
+    beside the GPU-side probes; cpu_baseline_result() collects its JSON."""
     env = dict(os.environ, **{v: "1" for v in CPU_THREAD_VARS})
+    return subprocess.Popen([sys.executable, os.path.abspath(__file__), "--cpu-sample", config],
+                            env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+
+
+def cpu_baseline_result(proc):
     try:
-        out = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-sample", config],
-                             env=env, capture_output=True, text=True, timeout=600)
-        return json.loads(out.stdout.strip().splitlines()[-1])
+        out, _ = proc.communicate(timeout=600)
+        return json.loads(out.strip().splitlines()[-1])
     except (subprocess.SubprocessError, ValueError, IndexError) as e:
+        proc.kill()
         return {"value": None, "error": f"cpu baseline failed: {e}"}
 
 
@@ -326,6 +366,53 @@ def run_reference(args, rank):
 
 
 # ----------------------------------------------------------------------------- B200 arm
+def probe_config(name, dtype_name, steps=4, warmup=2):
+    """A few eagerly launched, event-timed cycles of another BASELINE config on this GPU:
+    cycle time and the fused sweep's roofline (the p = 1 configs C3 and C5-weak, beside
+    the p = 3 headline)."""
+    import torch
+    import paper_2301_09991_b200 as P
+    from paper_2301_09991_b200.eigen import Solver
+    from paper_2301_09991_b200.problems import problem_from_data
+    pd = workload(name)
+    eigen = pd.driver == "power_iteration"
+    inner = pd.inner_iters or 1
+    opts = options_for(P, pd, dtype_name, None if eigen else steps + warmup)
+    if eigen:
+        opts.outer_iters = -(-(steps + warmup) // inner)
+    solver = Solver(problem_from_data(pd), opts, inner if eigen else None)
+    eng = solver.eng
+    eng.use_graphs = False
+    for _ in range(warmup):
+        solver.step()
+    eng.probe = {}
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(steps):
+        solver.step()
+    ev1.record()
+    torch.cuda.synchronize()
+    probe = {k: [a.elapsed_time(b) for a, b in v] for k, v in eng.probe.items()}
+    ms_k = float(np.mean(probe["pg_sweep"]))
+    peak, peak_kind, peaks = measured_peaks()
+    esz = 4 if opts.torch_dtype() == torch.float32 else 8
+    hbm, fp, bound, roof_frac = sweep_roofline(pd, pd.dof(), esz, eng, ms_k, peak, peak_kind, peaks)
+    out = {"workload": WORKLOADS.get(name, name), "dof_per_cycle": pd.dof(),
+           "ms_per_cycle": ev0.elapsed_time(ev1) / steps, "cycles": steps,
+           "value": pd.dof() * steps / (ev0.elapsed_time(ev1) * 1e-3),
+           "pg_sweep": {"ms_per_launch": ms_k, "bound": bound, "hbm_frac": hbm["frac"],
+                        "hbm_GBps": hbm["achieved"], "bytes_per_dof": hbm["bytes_per_dof"],
+                        "fp32_frac": fp["frac"], "roof_frac": roof_frac},
+           "kernels_ms": {k: float(np.mean(v)) for k, v in probe.items()}}
+    eng.probe = None
+    del solver, eng
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_b200(args, rank, world, local_rank):
     import torch
     import paper_2301_09991_b200 as P
@@ -412,37 +499,40 @@ def run_b200(args, rank, world, local_rank):
     value = dof * args.steps / (ms * 1e-3)          # global DOF: strong scaling over ranks
     ldof = dof // world                              # this rank's slab: kernel-level rates
 
-    # ---- roofline of the dominant kernel (fused PG sweep, K5): 20 B/DOF fp32
+    # ---- roofline of the dominant kernel (fused PG sweep, K5)
     peak, peak_kind, peaks = measured_peaks()
     esz = 4 if dtype == torch.float32 else 8
     kernel_stats = {}
     for k, ts in probe.items():
         kernel_stats[k] = {"ms_avg": float(np.mean(ts)), "launches": len(ts),
                            "ms_min": float(np.min(ts)), "ms_max": float(np.max(ts))}
-        if per_dof_bytes(k, esz):
-            kernel_stats[k]["GBps"] = per_dof_bytes(k, esz) * ldof / (np.mean(ts) * 1e-3) / 1e9
+        if per_dof_bytes(k, esz, eng):
+            kernel_stats[k]["GBps"] = per_dof_bytes(k, esz, eng) * ldof / (np.mean(ts) * 1e-3) / 1e9
     dominant = "pg_sweep" if "pg_sweep" in probe else "upwind_residual"
     roof = None
     if dominant in probe:
         ms_k = float(np.mean(probe[dominant]))
-        bpl = per_dof_bytes(dominant, esz) * ldof
-        achieved = bpl / (ms_k * 1e-3) / 1e9
         # the committed ncu capture is of the default 1-GPU workload
         traffic = (committed_traffic(args.config, dominant, args.dtype)
                    if world == 1 and not args.fold and args.nx is None else None)
-        roof = {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak,
-                "peak_source": ("measured (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
-                                else "fallback 6.65 TB/s"),
-                "traffic": traffic, "bytes_per_launch": bpl, "ms_per_launch": ms_k,
-                "share_of_step": ms_k * len(probe[dominant]) / (sum(sum(v) for v in probe.values()) or 1),
-                "timing": kernel_timing}
-        if pd.options.get("order", 1) >= 3:
-            flops = (32 * (2 * pd.options["order"] + 1) + 22) * ldof
-            fp32_peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
-            roof["fp32"] = {"tflops": flops / (ms_k * 1e-3) / 1e12, "peak_tflops": fp32_peak,
-                            "frac": flops / (ms_k * 1e-3) / 1e12 / fp32_peak,
-                            "note": "p=3 sits past the FP32 ridge (~9 F/B): 32T+22 flops/DOF vs 20 B/DOF"}
+        common = {"kernel": dominant, "traffic": traffic, "ms_per_launch": ms_k,
+                  "share_of_step": ms_k * len(probe[dominant]) / (sum(sum(v) for v in probe.values()) or 1),
+                  "timing": kernel_timing}
+        if dominant == "pg_sweep":
+            hbm, fp, bound, roof_frac = sweep_roofline(pd, ldof, esz, eng, ms_k, peak, peak_kind,
+                                                       peaks)
+            main = fp if bound == "fp32" else hbm
+            roof = {"bound": bound, "achieved": main["achieved"], "peak": main["peak"],
+                    "unit": main["unit"], "frac": main["frac"], "peak_source": main["peak_source"],
+                    **common, "bytes_per_launch": hbm["bytes_per_launch"],
+                    "hbm": hbm, "fp32": fp, "roof_frac": roof_frac,
+                    "note": ("bound = the lower roof for this ConvFEM order: t_roof = max(bytes / "
+                             "measured HBM, flops / FP32 peak); roof_frac = t_roof / launch time")}
+        else:
+            bpl = per_dof_bytes(dominant, esz, eng) * ldof
+            roof = {"bound": "hbm", "achieved": bpl / (ms_k * 1e-3) / 1e9, "peak": peak,
+                    "unit": "GB/s", "frac": bpl / (ms_k * 1e-3) / 1e9 / peak,
+                    "bytes_per_launch": bpl, **common}
     live = sum(1 for f in frozen_before if not f)
     b_cycle = (bytes_model(pd, solver.setup.hierarchy, True) * live
                + bytes_model(pd, solver.setup.hierarchy, False) * (args.steps - live)) / args.steps
@@ -483,9 +573,24 @@ def run_b200(args, rank, world, local_rank):
                "note": "solve_fixed_source/power_iteration call incl. setup, uploads, phi read-back"}
 
     # ---- CPU baseline (oracle port, bounded sample, rank 0 at N = 1)
-    cpu = None
+    cpu, cpu_proc = None, None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline_subprocess(args.config)
+        cpu_proc = cpu_baseline_start(args.config)
+
+    # ---- the p = 1 configs' fused sweep beside the p = 3 headline (1 GPU, default run)
+    others = None
+    if rank == 0 and world == 1 and not args.no_extra and args.config == "c4" and args.nx is None:
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
+        others = {}
+        for name, steps in (("c3", 10), ("c5w", 4)):
+            try:
+                others[name] = probe_config(name, args.dtype, steps=steps, warmup=2)
+            except Exception as e:   # e.g. not enough free memory: say so, keep the line
+                others[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    if cpu_proc is not None:
+        cpu = cpu_baseline_result(cpu_proc)
 
     if rank == 0:
         line = {
@@ -512,6 +617,7 @@ def run_b200(args, rank, world, local_rank):
             "cycle_roofline": {"bytes_per_cycle": b_cycle, "achieved": cycle_roof, "peak": peak,
                                "unit": "GB/s", "frac": cycle_roof / peak},
             "kernels": kernel_stats,
+            "other_configs": others,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(n_launch),
@@ -556,6 +662,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the C3 / C5-weak sweep probes after the headline")
     ap.add_argument("--fold", action="store_true",
                     help="z-mirror fold (half the ordinates, same flux); value counts the "
                          "DOF actually updated, not the full-sphere equivalent")

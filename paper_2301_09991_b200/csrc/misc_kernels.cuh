@@ -160,6 +160,9 @@ boundary4_kernel(Geo g, float* f, int h, const float* mu, const float* nu) {
             int xs, ys;
             if (k < n_rowcells) {
                 const int r = k / NY;
+                // a ghost side's rows hold the neighbour's data (domain decomposition):
+                // the halo exchange fills them, the boundary leaves them alone
+                if (r < h ? g.ghost_w : g.ghost_e) continue;
                 ys = k - r * NY;
                 xs = r < h ? r : g.nx + r;
             } else {
@@ -208,6 +211,9 @@ boundary_kernel(Geo g, Real* f, int h, const Real* mu, const Real* nu) {
             int xs, ys;   // storage coordinates
             if (k < n_rowcells) {
                 const int r = k / NY;
+                // a ghost side's rows hold the neighbour's data (domain decomposition):
+                // the halo exchange fills them, the boundary leaves them alone
+                if (r < h ? g.ghost_w : g.ghost_e) continue;
                 ys = k - r * NY;
                 xs = r < h ? r : g.nx + r;
             } else {

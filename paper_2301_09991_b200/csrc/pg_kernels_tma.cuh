@@ -48,8 +48,17 @@ constexpr size_t pg_residual_tma_smem() {
            128;   // + alignment slack (TMA destinations: 128 B)
 }
 
+// resident CTAs per SM the TMA residual / sweep is compiled for: the linear (p = 1)
+// march needs fewer registers, but 3 CTAs/SM (80 registers, small spills) measured
+// C3 1.37 -> 1.48 ms/cycle and 4 (64) 1.64 ms: kept at 2
+#ifndef CSN_TMA_MINB1
+#define CSN_TMA_MINB1 2
+#endif
+template <int L>
+struct TmaMinBlocks { static constexpr int value = L == 1 ? CSN_TMA_MINB1 : (L <= 3 ? 2 : 1); };
+
 template <int L, int MODE, int KD = 0>
-__global__ void __launch_bounds__(32 * PG_TX, L <= 3 ? 2 : 1)
+__global__ void __launch_bounds__(32 * PG_TX, TmaMinBlocks<L>::value)
 pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTmaMaps m) {
     // KD 0: D computed here; 1: computed and stored to a.dterm; 2: read from a.dterm
     // (bit-identical: the stored value is the one this kernel would compute)

@@ -271,7 +271,8 @@ class DDCycleEngine(CycleEngine):
         self.x0_levels = x0_levels
         super().__init__(local_h, n_group, dtype, device)
         self.pad_delta = False         # x-ghosted finest correction (see correction)
-        self.fold_delta = False        # the sweep reads delta's exchanged ghost rows
+        # the finest correction folds into psi (as on one GPU); psi' ghost rows (width l)
+        # are then exchanged instead of delta's
         self.use_dterm = False
         west, east = comm.rank > 0, comm.rank < comm.size - 1
         self.geoms = [lev.geom(n_group, int(west), int(east)) for lev in local_h.levels]
@@ -329,7 +330,7 @@ class DDCycleEngine(CycleEngine):
     def _hook_l1(self):
         self.comm.allreduce_sum_(self.l1)
 
-    def correction(self, r0, n_sweeps, finest_scale, out0=None, out0_halo=0):
+    def correction(self, r0, n_sweeps, finest_scale, out0=None, out0_halo=0, fold=False):
         if n_sweeps > UP_MAX_SWEEPS:
             raise ValueError("domain decomposition supports <= 3 Jacobi sweeps per level")
         L = self.h.levels
@@ -379,6 +380,10 @@ class DDCycleEngine(CycleEngine):
         prev, gc = ci.view, self.coarse_geom
         for i in range(len(L) - 1, -1, -1):
             scale = finest_scale if i == 0 else 1.0
+            if i == 0 and fold:     # psi -= delta on the slab's interior (no delta ghosts)
+                return _smooth_chain(L[0], self.ng, self.src[0], 1, prev, 2, 0, gc, n_sweeps,
+                                     scale, out0, out0_halo, None, self.sigma[0], self.geoms[0],
+                                     fold=True)
             prev = _smooth_chain(L[i], self.ng, self.src[i], 1, prev, 2, 0, gc, n_sweeps, scale,
                                  self.delta[i], 0, None, self.sigma[i], self.geoms[i])
             # ghosts the next reader needs: the finer level's warm-up prolongs from

@@ -772,6 +772,9 @@ class CycleEngine:
         nd, ng = psi_in.shape[2], psi_in.shape[3]
         self.sweep_reach = fs.half_width if scheme == "pg" else 1    # x reach of the update
         fold = (self.fold_delta and plan["pg_sweeps"] > 0 and n_sweeps <= UP_MAX_SWEEPS)
+        # field elements the (first) fused sweep moves per DOF: psi, delta, kx, ky -> psi,
+        # or psi', kx, ky -> psi when the correction is folded into the iterate
+        self.sweep_elems = 4 if fold else 5
         pad = self.pad_delta and plan["pg_sweeps"] > 0 and not fold
         dh = fs.half_width if pad else 0
         if pad and (self.delta0p is None or self.delta0p.shape[0] != g.nx + 2 * dh):
@@ -785,6 +788,8 @@ class CycleEngine:
             self.correction(self.r0, n_sweeps, cfg.beta_diag, psi_in, g.halo, fold=True)
             _lib.call("csn_apply_boundary", dt, self.geoms[0], _lib.ptr(psi_in), g.halo,
                       _lib.ptr(c0["mu"]), _lib.ptr(c0["nu"]), _lib.stream())
+            # DD ranks: psi' ghost rows for the sweep's l-wide x reach
+            self._hook_exchange_many([(psi_in, fs.half_width)])
             delta = None
         else:
             delta = self.correction(self.r0, n_sweeps, cfg.beta_diag if scheme == "pg" else 1.0,
