@@ -57,11 +57,13 @@ constexpr size_t pg_residual_tma_smem() {
 template <int L>
 struct TmaMinBlocks { static constexpr int value = L == 1 ? CSN_TMA_MINB1 : (L <= 3 ? 2 : 1); };
 
-template <int L, int MODE, int KD = 0>
+template <int L, int MODE, int KD = 0, bool G1 = false>
 __global__ void __launch_bounds__(32 * PG_TX, TmaMinBlocks<L>::value)
 pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTmaMaps m) {
     // KD 0: D computed here; 1: computed and stored to a.dterm; 2: read from a.dterm
-    // (bit-identical: the stored value is the one this kernel would compute)
+    // (bit-identical: the stored value is the one this kernel would compute).
+    // G1: one group and a per-cell source (the 1-group configs): sigma and q of a cell
+    // are one scalar load each, at unit stride in y
     constexpr bool SWEEP = MODE == PG_SWEEP || MODE == PG_SWEEPF;
     constexpr bool DSUB = MODE == PG_SWEEP;       // psi' = psi - delta formed per read
     constexpr bool EMA = MODE == PG_RESID_EMA;
@@ -81,7 +83,8 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
     // space (a uintptr_t round trip would turn every ring read into a generic LD)
     float* sm = reinterpret_cast<float*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
     __shared__ double red[32];
-    __shared__ __align__(8) uint64_t full[S], empty[S];
+    __shared__ __align__(8) uint64_t full[S];
+    __shared__ unsigned relc[S];                   // warps done with each slot
 
     const Geo& g = a.g;
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -107,22 +110,24 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], PG_TX);           // one arrival per warp
+            relc[s] = 0u;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
+    // shared-window addresses of the ring and its barriers, once
+    const unsigned sm_s = smem_u32(sm), full_s = smem_u32(full);
     // producer: lead row ya - L + k of every field into slot s
     auto issue = [&](int k, int s) {
         const int yy = ya - L + k;
-        float* dst = sm + s * SLOT;
-        mbar_expect_tx(&full[s], TXB);
-        tma_load_3d(dst, &m.psi, &full[s], c0, yy + a.psi_h, x0 - L + a.psi_h);
-        tma_load_3d(dst + FS, &m.kx, &full[s], c0, yy + a.k_h, x0 - L + a.k_h);
-        tma_load_3d(dst + 2 * FS, &m.ky, &full[s], c0, yy + a.k_h, x0 - L + a.k_h);
-        if (DSUB) tma_load_3d(dst + 3 * FS, &m.aux, &full[s], c0, yy + a.delta_h, x0 - L + a.delta_h);
-        if (EMA) tma_load_3d(dst + 3 * FS, &m.aux, &full[s], c0, yy + a.avg_h, x0 + a.avg_h);
+        const unsigned dst = sm_s + s * (SLOT * 4), fb = full_s + 8 * s;
+        mbar_expect_tx_s(fb, TXB);
+        tma_load_3d_s(dst, &m.psi, fb, c0, yy + a.psi_h, x0 - L + a.psi_h);
+        tma_load_3d_s(dst + FS * 4, &m.kx, fb, c0, yy + a.k_h, x0 - L + a.k_h);
+        tma_load_3d_s(dst + 2 * FS * 4, &m.ky, fb, c0, yy + a.k_h, x0 - L + a.k_h);
+        if (DSUB) tma_load_3d_s(dst + 3 * FS * 4, &m.aux, fb, c0, yy + a.delta_h, x0 - L + a.delta_h);
+        if (EMA) tma_load_3d_s(dst + 3 * FS * 4, &m.aux, fb, c0, yy + a.avg_h, x0 + a.avg_h);
     };
 
     // epilogue pointers at y = 0 (per output only y * stride is added)
@@ -137,6 +142,7 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
                        : (a.r ? a.r + fidx(xs, 0, cs, g.ny, a.r_h, g.C) : nullptr);
     float* avg_p = EMA && act ? a.avg + fidx(x, 0, cs, g.ny, a.avg_h, g.C) : nullptr;
     const float2 beta2 = bc2(a.beta);
+    const bool refine = a.refine_div != 0;
     const float2 strm2 = a.strm ? make_float2(a.strm[n0], a.strm[n1]) : bc2(0.f);
     const int oy0 = max(ya, 0), oy1 = yb;
     const int lane_off = ty * CC + 2 * tx;          // this lane's pair in a staged row
@@ -148,9 +154,9 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
     float2 dN = bc2(0.f);
     if (KD == 2 && act) dN = ld2(dt_p + (int64_t)ya * g.C);
 
-    if (producer) {
+    if (producer) {          // every slot's first row; refills come from the releases
 #pragma unroll
-        for (int k = 0; k < P; ++k)
+        for (int k = 0; k < S; ++k)
             if (k < nsteps) issue(k, k);
     }
     double l1 = 0.0;
@@ -158,8 +164,13 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
     unsigned fpar = 0;     // parity of the current fill of `slot`
     float2 sgN = bc2(0.f), qN = bc2(0.f);
     if (act) {
-        sgN = make_float2(sig0[ya * g.ng], sig1[ya * g.ng]);
-        qN = make_float2(q0[ya * qst], q1[ya * qst]);
+        if (G1) {
+            sgN = bc2(sig0[ya]);
+            qN = bc2(q0[ya]);
+        } else {
+            sgN = make_float2(sig0[ya * g.ng], sig1[ya * g.ng]);
+            qN = make_float2(q0[ya * qst], q1[ya * qst]);
+        }
     }
 
 #define TMA_STEP(K, SK, OUT, Y, SLOTC)                                                \
@@ -168,11 +179,16 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
         const int ss_ = (SLOTC) >= 0 ? (SLOTC) : slot;                                \
         float2 sg_ = sgN, q_ = qN, dd_ = dN;                                          \
         if ((OUT) && act && (Y) + 1 < yb) {                                           \
-            sgN = make_float2(sig0[((Y) + 1) * g.ng], sig1[((Y) + 1) * g.ng]);       \
-            qN = make_float2(q0[((Y) + 1) * qst], q1[((Y) + 1) * qst]);              \
+            if (G1) {                                                                 \
+                sgN = bc2(sig0[(Y) + 1]);                                             \
+                qN = bc2(q0[(Y) + 1]);                                                \
+            } else {                                                                  \
+                sgN = make_float2(sig0[((Y) + 1) * g.ng], sig1[((Y) + 1) * g.ng]);   \
+                qN = make_float2(q0[((Y) + 1) * qst], q1[((Y) + 1) * qst]);          \
+            }                                                                         \
             if (KD == 2) dN = ld2(dt_p + (int64_t)((Y) + 1) * g.C);                  \
         }                                                                             \
-        mbar_wait(&full[ss_], fpar);                                                   \
+        mbar_wait_s(full_s + 8 * ss_, fpar);                                           \
         const float* buf_ = sm + ss_ * SLOT;                                           \
         if (EMA && avg_p) {                                                           \
             const int yl_ = ya - L + k_;                                              \
@@ -241,7 +257,7 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
                 const float2 d_ = mul2(beta2, add2(strm2, sg_));                      \
                 const float2 inv_ = make_float2(rcp_nr(d_.x), rcp_nr(d_.y));          \
                 float2 qt_ = mul2(r_, inv_);                                          \
-                if (a.refine_div)                                                     \
+                if (refine)                                                           \
                     qt_ = fma2(fma2(make_float2(-d_.x, -d_.y), qt_, r_), inv_, qt_);  \
                 st2(o_p + (int64_t)y_ * g.C, sub2(pc_, qt_));                         \
             } else {                                                                  \
@@ -249,15 +265,19 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
                 l1 += fabs((double)r_.x) + fabs((double)r_.y);                        \
             }                                                                         \
         }                                                                             \
-        if (k_ >= L) {                       /* last read of the centre row's slot */ \
+        if ((OUT) || k_ >= L) {              /* last read of the centre row's slot */ \
             __syncwarp();                                                             \
-            if (tx == 0) mbar_arrive(&empty[cs_]);                                    \
-        }                                                                             \
-        if (producer && k_ + P < nsteps) {                                            \
-            const int is_ = ss_ + P >= S ? ss_ + P - S : ss_ + P;                  \
-            const int fill_ = (k_ + P) / S;                                           \
-            if (fill_ >= 1) mbar_wait(&empty[is_], (unsigned)((fill_ - 1) & 1));      \
-            issue(k_ + P, is_);                                                       \
+            if (tx == 0) {                                                            \
+                /* the last warp to release the slot refills it (row k - L + S): no   \
+                   warp ever waits for the others to free a slot */                   \
+                if (atomicAdd(&relc[cs_], 1u) == PG_TX - 1) {                         \
+                    relc[cs_] = 0u;                                                   \
+                    if (k_ - L + S < nsteps) {                                        \
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  \
+                        issue(k_ - L + S, cs_);                                       \
+                    }                                                                 \
+                }                                                                     \
+            }                                                                         \
         }                                                                             \
         slot = ss_ + 1; if (slot == S) { slot = 0; fpar ^= 1u; }                                 \
     }
