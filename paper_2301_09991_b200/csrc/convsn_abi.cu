@@ -36,7 +36,7 @@ int g_tune_upwind_div = 3;
 int g_tune_sweep_div = 1;
 int g_tune_pg_tma = 1;
 int g_tune_upwind_tma = 0;
-int g_tune_k2_tma = 0;   // TMA-staged K2b: 2.18 ms vs 2.09 ms cp.async on C4
+int g_tune_k2_tma = 1;   // TMA-staged K2b (last releaser refills its ring slot): C4 K2 4.04 -> 3.93 ms; the cp.async K2b was faster before that refill scheme (2.09 vs 2.18 ms)
 int g_tune_k2_ws = 0;
 int g_tune_pg_xb = 0;   // x-blocked residual / sweep (warps per CTA: 4 or 8; 0 = off)   // one-pass K2: 5.0 ms vs 4.2 ms split on C4 (stage 2 starved)
 
@@ -361,7 +361,8 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
             dim3 grid(gx, gy, (int)cdiv(g->ny + 2 * L, a.ly));
             // TMA staging of the workspace rows (k2_tma), else the cp.async stager
             KcoefMaps km;     // the workspace is a field with halo gh = 2l
-            const bool tk = g_tune_k2_tma && field_map(&km.gx, gxp, g, gh, PG_TX + 2 * L) &&
+            // k2_tma: 1 = TMA K2b at L >= 3 (C2, p = 2: 0.159 vs 0.166 ms cp.async), 2 = always
+            const bool tk = (g_tune_k2_tma == 2 || (g_tune_k2_tma == 1 && L >= 3)) && field_map(&km.gx, gxp, g, gh, PG_TX + 2 * L) &&
                             field_map(&km.gy, gyp, g, gh, PG_TX + 2 * L);
             if (tk) launch_pg_kcoef_tma<L>(grid, block, st, a, km, gh);
             else if (vec) launch_pg_kcoef_x2<L, V>(grid, block, st, a, gxp, gyp, gh);

@@ -335,7 +335,8 @@ pg_kcoef_tma_kernel(const PGKArgs<float> a, const __grid_constant__ KcoefMaps m,
     constexpr unsigned TXB = 2 * FS * sizeof(float);
     extern __shared__ __align__(128) unsigned char smraw[];
     float* sm = reinterpret_cast<float*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
-    __shared__ __align__(8) uint64_t full[S], empty[S];
+    __shared__ __align__(8) uint64_t full[S];
+    __shared__ unsigned relc[S];                   // warps done with each slot
 
     const Geo& g = a.g;
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -360,7 +361,7 @@ pg_kcoef_tma_kernel(const PGKArgs<float> a, const __grid_constant__ KcoefMaps m,
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], PG_TX);
+            relc[s] = 0u;
         }
         fence_mbarrier_init();
     }
@@ -372,9 +373,9 @@ pg_kcoef_tma_kernel(const PGKArgs<float> a, const __grid_constant__ KcoefMaps m,
         tma_load_3d(dst, &m.gx, &full[s], c0, yy + gh, x0 - L + gh);
         tma_load_3d(dst + FS, &m.gy, &full[s], c0, yy + gh, x0 - L + gh);
     };
-    if (producer) {
+    if (producer) {          // every slot's first row; refills come from the releases
 #pragma unroll
-        for (int k = 0; k < P; ++k)
+        for (int k = 0; k < S; ++k)
             if (k < nsteps) issue(k, k);
     }
     float2 r2x[T], r2y[T];   // M_x psi_x, M_x psi_y by lead row (step mod T)
@@ -422,13 +423,13 @@ pg_kcoef_tma_kernel(const PGKArgs<float> a, const __grid_constant__ KcoefMaps m,
         }                                                                                 \
         if (k_ >= L) {                    /* last read of the centre row's slot */        \
             __syncwarp();                                                                 \
-            if (tx == 0) mbar_arrive(&empty[cs_]);                                        \
-        }                                                                                 \
-        if (producer && k_ + P < nsteps) {                                                \
-            const int is_ = slot + P >= S ? slot + P - S : slot + P;                      \
-            const int fill_ = (k_ + P) / S;                                               \
-            if (fill_ >= 1) mbar_wait(&empty[is_], (unsigned)((fill_ - 1) & 1));          \
-            issue(k_ + P, is_);                                                           \
+            if (tx == 0 && atomicAdd(&relc[cs_], 1u) == PG_TX - 1) {                      \
+                relc[cs_] = 0u;                   /* the last releaser refills it */      \
+                if (k_ - L + S < nsteps) {                                                \
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");          \
+                    issue(k_ - L + S, cs_);                                               \
+                }                                                                         \
+            }                                                                             \
         }                                                                                 \
         if (++slot == S) { slot = 0; fpar ^= 1u; }                                        \
     }
