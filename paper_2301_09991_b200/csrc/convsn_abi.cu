@@ -35,7 +35,7 @@ int g_tune_upwind_x2 = 1;
 int g_tune_upwind_div = 3;
 int g_tune_sweep_div = 1;
 int g_tune_pg_tma = 1;
-int g_tune_upwind_tma = 0;
+int g_tune_upwind_tma = 1;   // TMA-staged smoother columns (last releaser refills): C4 correction 1.99 -> 1.75 ms
 int g_tune_k2_tma = 1;   // TMA-staged K2b (last releaser refills its ring slot): C4 K2 4.04 -> 3.93 ms; the cp.async K2b was faster before that refill scheme (2.09 vs 2.18 ms)
 int g_tune_k2_ws = 0;
 int g_tune_pg_xb = 0;   // x-blocked residual / sweep (warps per CTA: 4 or 8; 0 = off)   // one-pass K2: 5.0 ms vs 4.2 ms split on C4 (stage 2 starved)
@@ -452,10 +452,11 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
             const int gz = (int)cdiv(g->nx, a.xchunk);
             dim3 grid(gx, gy, gz), block(32, UPX_SPB);
             // TMA-staged columns (upwind_smooth_tma_kernel) where its layout applies
-            // (default off: measured on C4 1.18 ms vs 1.15 ms for the register kernel —
-            // both sit at ~47% of DRAM bandwidth with 16 warps/SM, so the deeper
-            // prefetch does not pay for its shared-memory reads)
-            if (g_tune_upwind_tma && !fold && g1 && a.exact_div == 3 && init_mode != 1 && g->na >= 8 &&
+            // (default on since the last warp to release a column slot refills it: the
+            // producer thread no longer waits for every warp each step — C4 correction
+            // 1.99 -> 1.75 ms; with producer waits it had measured 1.18 vs 1.15 ms for
+            // the register kernel)
+            if (g_tune_upwind_tma && g1 && a.exact_div == 3 && init_mode != 1 && g->na >= 8 &&
                 g->na <= 32 && g->ny % 4 == 0 && !g->ghost_w && !g->ghost_e &&
                 (init_mode == 0 || (init_h == 0 && a.angle_coarsens))) {
                 UpTmaMaps maps;
