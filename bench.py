@@ -133,7 +133,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- workload
-def workload(name, nx=None, world=1):
+def workload(name, nx=None, world=1, n_a=None, slabs=None):
     """BASELINE config by name; c5w is the weak-scaling C5 variant (512 x 512 cells per
     rank, stacked along x), c5 the full 1024 x 1024 C5 (strong scaling, >= 4 GPUs: one
     fp32 field is 60.8 GB)."""
@@ -145,9 +145,12 @@ def workload(name, nx=None, world=1):
     if name == "c3":
         return B.c3()
     if name == "c4":
-        return B.c4() if nx is None else B.c4(nx=nx, blocks=nx // 16)
+        kw = {"n_a": n_a} if n_a else {}
+        return B.c4(**kw) if nx is None else B.c4(nx=nx, blocks=nx // 16, **kw)
     if name == "c5w":
-        return B.c5_weak(world)
+        # slabs: build the weak problem of that many ranks whatever the world size (the
+        # single-domain reference of a DD plumbing check); n_a: fewer ordinates (checks)
+        return B.c5_weak(slabs or world, **({"n_a": n_a} if n_a else {}))
     if name == "c5":
         if world < 4:
             raise SystemExit("c5 (1024^2 x 2048 ordinates x 7 groups, 60.8 GB per fp32 "
@@ -426,7 +429,7 @@ def run_b200(args, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
-    pd = workload(args.config, args.nx, world)
+    pd = workload(args.config, args.nx, world, args.na, args.slabs)
     total = args.warmup + args.steps
     eigen = pd.driver == "power_iteration"
     inner = pd.inner_iters or 1
@@ -514,7 +517,8 @@ def run_b200(args, rank, world, local_rank):
         ms_k = float(np.mean(probe[dominant]))
         # the committed ncu capture is of the default 1-GPU workload
         traffic = (committed_traffic(args.config, dominant, args.dtype)
-                   if world == 1 and not args.fold and args.nx is None else None)
+                   if world == 1 and not args.fold and args.nx is None and args.na is None
+                   else None)
         common = {"kernel": dominant, "traffic": traffic, "ms_per_launch": ms_k,
                   "share_of_step": ms_k * len(probe[dominant]) / (sum(sum(v) for v in probe.values()) or 1),
                   "timing": kernel_timing}
@@ -579,7 +583,8 @@ def run_b200(args, rank, world, local_rank):
 
     # ---- the p = 1 configs' fused sweep beside the p = 3 headline (1 GPU, default run)
     others = None
-    if rank == 0 and world == 1 and not args.no_extra and args.config == "c4" and args.nx is None:
+    if (rank == 0 and world == 1 and not args.no_extra and args.config == "c4" and args.nx is None
+            and args.na is None):
         import gc
         gc.collect()
         torch.cuda.empty_cache()
@@ -658,6 +663,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4")
     ap.add_argument("--nx", type=int, default=None, help="override the cell count (c4 only)")
+    ap.add_argument("--na", type=int, default=None,
+                    help="override n_a (c4, c5w; plumbing checks, not a BASELINE config)")
+    ap.add_argument("--slabs", type=int, default=None,
+                    help="c5w: the weak problem of this many ranks, (512 S) x 512, on any world")
     ap.add_argument("--dtype", default="float32")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")

@@ -368,7 +368,10 @@ class DDCycleEngine(CycleEngine):
             lo, hi = max(x0 - GX, 0), min(x0 + w + GX, cl.grid.nx)
             ci.full[lo - (x0 - GX):hi - (x0 - GX)].copy_(dc[lo:hi])
 
+        t = self._t0()
         self._run_graphed(("restrict", r0.data_ptr()), restrict_local)
+        self._t1("corr.restrict", t)
+        t = self._t0()
         full = comm.allgather_x(self._local_coarse)
         # every distributed level's source ghosts (the smoother's H-column warm-up) in one
         # grouped exchange, in flight while the gathered coarse levels are solved
@@ -377,19 +380,24 @@ class DDCycleEngine(CycleEngine):
         self._coarse_in.copy_(full)
         self._run_graphed(("coarse", n_sweeps), coarse_solve)
         src_x.wait()
+        self._t1("corr.gather+coarse", t)
         prev, gc = ci.view, self.coarse_geom
         for i in range(len(L) - 1, -1, -1):
             scale = finest_scale if i == 0 else 1.0
+            t = self._t0()
             if i == 0 and fold:     # psi -= delta on the slab's interior (no delta ghosts)
-                return _smooth_chain(L[0], self.ng, self.src[0], 1, prev, 2, 0, gc, n_sweeps,
-                                     scale, out0, out0_halo, None, self.sigma[0], self.geoms[0],
-                                     fold=True)
+                out = _smooth_chain(L[0], self.ng, self.src[0], 1, prev, 2, 0, gc, n_sweeps,
+                                    scale, out0, out0_halo, None, self.sigma[0], self.geoms[0],
+                                    fold=True)
+                self._t1("corr.smooth0", t)
+                return out
             prev = _smooth_chain(L[i], self.ng, self.src[i], 1, prev, 2, 0, gc, n_sweeps, scale,
                                  self.delta[i], 0, None, self.sigma[i], self.geoms[i])
             # ghosts the next reader needs: the finer level's warm-up prolongs from
             # (H + 1) / 2 coarse columns; the fused sweep reads l columns of the finest
             w = (UP_MAX_SWEEPS + 1) // 2 if i > 0 else min(GX, self.sweep_reach)
             comm.exchange(self.delta_g[i].full, w, GX)
+            self._t1(f"corr.smooth{i}", t)
             gc = self.geoms[i]
         return prev
 
