@@ -178,7 +178,8 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
     constexpr bool X2 = sizeof(Real) == 4;
     const int gx = (int)cdiv(g->nx, PG_TX);
     const int gy = (int)cdiv((int64_t)g->nd * g->ng, X2 ? X2_CC : PG_CC);
-    a.ly = pick_ly((int64_t)gx * gy, g->ny, T);
+    // y chunks a multiple of the TMA march's unroll (2T at L = 1, see TmaRing)
+    a.ly = pick_ly((int64_t)gx * gy, g->ny, X2 && L == 1 ? 2 * T : T);
     const int gz = (int)cdiv(g->ny, a.ly);
     a.partials = (l1 || partials) ? partials : nullptr;
     dim3 grid(gx, gy, gz), block(PG_CC, PG_TX);

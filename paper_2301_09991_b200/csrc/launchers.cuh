@@ -40,14 +40,18 @@ template <int L, int MODE, int KD>
 void launch_pg_resid_tma(dim3 grid, dim3 block, cudaStream_t st, const PGResidArgs<float>& a,
                          const PGTmaMaps& maps) {
     constexpr size_t sm = pg_residual_tma_smem<L, MODE>();
-#ifndef CSN_NO_G1
     if (KD == 0 && a.g.ng == 1 && !a.q_per_dof) {       // 1 group, per-cell source
         static bool attr1 = false;
-        if (!attr1) { set_smem(pg_residual_tma_kernel<L, MODE, KD, true>, sm); attr1 = true; }
-        pg_residual_tma_kernel<L, MODE, KD, true><<<grid, block, sm, st>>>(a, maps);
+        if (!attr1) { set_smem(pg_residual_tma_kernel<L, MODE, KD, 1>, sm); attr1 = true; }
+        pg_residual_tma_kernel<L, MODE, KD, 1><<<grid, block, sm, st>>>(a, maps);
         return;
     }
-#endif
+    if (KD == 0 && a.g.ng == 2 && !a.q_per_dof) {       // 2 groups, per-cell source
+        static bool attr2 = false;
+        if (!attr2) { set_smem(pg_residual_tma_kernel<L, MODE, KD, 2>, sm); attr2 = true; }
+        pg_residual_tma_kernel<L, MODE, KD, 2><<<grid, block, sm, st>>>(a, maps);
+        return;
+    }
     static bool attr = false;
     if (!attr) { set_smem(pg_residual_tma_kernel<L, MODE, KD>, sm); attr = true; }
     pg_residual_tma_kernel<L, MODE, KD><<<grid, block, sm, st>>>(a, maps);

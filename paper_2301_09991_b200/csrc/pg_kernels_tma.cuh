@@ -38,8 +38,13 @@ template <int L, int MODE>
 struct TmaRing {
     static constexpr int FS = (PG_TX + 2 * L) * X2_CC;
     static constexpr int SLOT = 3 * FS + (MODE == PG_SWEEP ? FS : MODE == PG_RESID_EMA ? PG_TX * X2_CC : 0);
-    static constexpr int PREFETCH = L > 3 ? 2 : 3;   // 4-5 measured slower (C4: spills, less L1)
+    // L = 3: S = T = 7 (4-5 rows ahead measured slower: spills, less L1); L = 1: S = 2T = 6
+    // (prefetch depth 3-7 measured equal on C3, C5-weak; S a multiple of T keeps the ring
+    // slot of every unrolled step a compile-time constant)
+    static constexpr int PREFETCH = L > 3 ? 2 : (L == 1 ? 4 : 3);
     static constexpr int S = L + 1 + PREFETCH;
+    static constexpr int T = 2 * L + 1;
+    static constexpr int U = S % T == 0 ? S : T;     // steps per unrolled march iteration
 };
 
 template <int L, int MODE>
@@ -57,13 +62,14 @@ constexpr size_t pg_residual_tma_smem() {
 template <int L>
 struct TmaMinBlocks { static constexpr int value = L == 1 ? CSN_TMA_MINB1 : (L <= 3 ? 2 : 1); };
 
-template <int L, int MODE, int KD = 0, bool G1 = false>
+template <int L, int MODE, int KD = 0, int GS = 0>
 __global__ void __launch_bounds__(32 * PG_TX, TmaMinBlocks<L>::value)
 pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTmaMaps m) {
     // KD 0: D computed here; 1: computed and stored to a.dterm; 2: read from a.dterm
     // (bit-identical: the stored value is the one this kernel would compute).
-    // G1: one group and a per-cell source (the 1-group configs): sigma and q of a cell
-    // are one scalar load each, at unit stride in y
+    // GS = 1 / 2: one or two groups and a per-cell source: sigma and q of a cell are one
+    // scalar (1 group) or one 8-byte pair load (2 groups: a lane's channel pair is the
+    // two groups of one direction) each, at a compile-time stride in y
     constexpr bool SWEEP = MODE == PG_SWEEP || MODE == PG_SWEEPF;
     constexpr bool DSUB = MODE == PG_SWEEP;       // psi' = psi - delta formed per read
     constexpr bool EMA = MODE == PG_RESID_EMA;
@@ -103,7 +109,8 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
     const int ya = blockIdx.z * a.ly;
     const int yb = min(g.ny, ya + a.ly);
     const bool act = x < g.nx && cval;
-    const int nsteps = 2 * L + (int)(((yb - ya) + T - 1) / T) * T;   // lead rows ya-L ...
+    constexpr int U = TmaRing<L, MODE>::U;
+    const int nsteps = 2 * L + (int)(((yb - ya) + U - 1) / U) * U;   // lead rows ya-L ...
     const bool producer = tid == 0;
 
     if (producer) {
@@ -164,9 +171,12 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
     unsigned fpar = 0;     // parity of the current fill of `slot`
     float2 sgN = bc2(0.f), qN = bc2(0.f);
     if (act) {
-        if (G1) {
+        if (GS == 1) {
             sgN = bc2(sig0[ya]);
             qN = bc2(q0[ya]);
+        } else if (GS == 2) {
+            sgN = ld2(sig0 + 2 * ya);
+            qN = ld2(q0 + 2 * ya);
         } else {
             sgN = make_float2(sig0[ya * g.ng], sig1[ya * g.ng]);
             qN = make_float2(q0[ya * qst], q1[ya * qst]);
@@ -179,9 +189,12 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
         const int ss_ = (SLOTC) >= 0 ? (SLOTC) : slot;                                \
         float2 sg_ = sgN, q_ = qN, dd_ = dN;                                          \
         if ((OUT) && act && (Y) + 1 < yb) {                                           \
-            if (G1) {                                                                 \
+            if (GS == 1) {                                                            \
                 sgN = bc2(sig0[(Y) + 1]);                                             \
                 qN = bc2(q0[(Y) + 1]);                                                \
+            } else if (GS == 2) {                                                     \
+                sgN = ld2(sig0 + 2 * ((Y) + 1));                                      \
+                qN = ld2(q0 + 2 * ((Y) + 1));                                         \
             } else {                                                                  \
                 sgN = make_float2(sig0[((Y) + 1) * g.ng], sig1[((Y) + 1) * g.ng]);   \
                 qN = make_float2(q0[((Y) + 1) * qst], q1[((Y) + 1) * qst]);          \
@@ -286,12 +299,12 @@ pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTma
 #pragma unroll
     for (int k = 0; k < 2 * L; ++k) TMA_STEP(k, (k + 1) % T, false, 0, k % S);
 
-    // S == T (p = 3): compile-time ring slot per unrolled step (see pg_residual_x2_kernel)
+    // S == U (a multiple of T): compile-time ring slot per unrolled step
     int kbase = 2 * L;
-    for (int y0 = ya; y0 < yb; y0 += T, kbase += T) {
+    for (int y0 = ya; y0 < yb; y0 += U, kbase += U) {
 #pragma unroll
-        for (int s = 0; s < T; ++s)
-            TMA_STEP(kbase + s, s, true, y0 + s, S == T ? (2 * L + s) % S : -1);
+        for (int s = 0; s < U; ++s)
+            TMA_STEP(kbase + s, s % T, true, y0 + s, S == U ? (2 * L + s) % S : -1);
     }
 #undef TMA_STEP
     if (!SWEEP && a.partials) {

@@ -316,7 +316,9 @@ class Solver:
             if self.in_phase == 0:       # freeze the fission source of this block
                 self._fis = self._frozen_fission(1.0 if boot else 1.0 / self.k)
             fission = self._fis
+        t = self.eng._t0()
         q = self._source(fission, self.in_phase == 0)
+        self.eng._t1("flux+source", t)
         # psi's halo is consistent: zero start / applied boundary at setup, then every
         # cycle ends with the boundary (uniform rescaling keeps it)
         res = self.eng.cycle(self.psi, q, self.setup.filters, opts.pg,
