@@ -362,8 +362,9 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
             dim3 grid(gx, gy, (int)cdiv(g->ny + 2 * L, a.ly));
             // TMA staging of the workspace rows (k2_tma), else the cp.async stager
             KcoefMaps km;     // the workspace is a field with halo gh = 2l
-            // k2_tma: 1 = TMA K2b at L >= 3 (C2, p = 2: 0.159 vs 0.166 ms cp.async), 2 = always
-            const bool tk = (g_tune_k2_tma == 2 || (g_tune_k2_tma == 1 && L >= 3)) && field_map(&km.gx, gxp, g, gh, PG_TX + 2 * L) &&
+            // k2_tma: 1 = TMA K2b except at L = 2 (C2: 0.159 vs 0.166 ms cp.async; C3 0.48 -> 0.45,
+            // C5-weak 25.1 -> 23.1 ms at L = 1), 2 = always
+            const bool tk = (g_tune_k2_tma == 2 || (g_tune_k2_tma == 1 && L != 2)) && field_map(&km.gx, gxp, g, gh, PG_TX + 2 * L) &&
                             field_map(&km.gy, gyp, g, gh, PG_TX + 2 * L);
             if (tk) launch_pg_kcoef_tma<L>(grid, block, st, a, km, gh);
             else if (vec) launch_pg_kcoef_x2<L, V>(grid, block, st, a, gxp, gyp, gh);
