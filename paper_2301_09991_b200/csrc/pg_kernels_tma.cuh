@@ -53,17 +53,23 @@ constexpr size_t pg_residual_tma_smem() {
            128;   // + alignment slack (TMA destinations: 128 B)
 }
 
-// resident CTAs per SM the TMA residual / sweep is compiled for: the linear (p = 1)
-// march needs fewer registers, but 3 CTAs/SM (80 registers, small spills) measured
-// C3 1.37 -> 1.48 ms/cycle and 4 (64) 1.64 ms: kept at 2
+// resident CTAs per SM the TMA residual / sweep is compiled for.  The linear (p = 1)
+// march fits 80 registers (3 CTAs/SM) without spills; measured per variant: the sweep
+// with generic group strides (GS = 0, e.g. the 7-group C5) gains 10% at 3 CTAs/SM
+// (C5-weak 17.5 -> 15.7 ms), the residual modes and the 1-/2-group specialisations lose
+// 2-4% (C3 sweep 0.237 -> 0.243 ms, residual 0.221 -> 0.230 ms), so only that variant
+// takes 3.  (4 CTAs/SM, 64 registers: spills, C3 1.37 -> 1.64 ms.)
 #ifndef CSN_TMA_MINB1
 #define CSN_TMA_MINB1 2
 #endif
-template <int L>
-struct TmaMinBlocks { static constexpr int value = L == 1 ? CSN_TMA_MINB1 : (L <= 3 ? 2 : 1); };
+template <int L, int MODE = PG_RESID, int GS = 1>
+struct TmaMinBlocks {
+    static constexpr bool sweep0 = (MODE == PG_SWEEP || MODE == PG_SWEEPF) && GS == 0;
+    static constexpr int value = L == 1 ? (sweep0 ? 3 : CSN_TMA_MINB1) : (L <= 3 ? 2 : 1);
+};
 
 template <int L, int MODE, int KD = 0, int GS = 0>
-__global__ void __launch_bounds__(32 * PG_TX, TmaMinBlocks<L>::value)
+__global__ void __launch_bounds__(32 * PG_TX, TmaMinBlocks<L, MODE, GS>::value)
 pg_residual_tma_kernel(const PGResidArgs<float> a, const __grid_constant__ PGTmaMaps m) {
     // KD 0: D computed here; 1: computed and stored to a.dterm; 2: read from a.dterm
     // (bit-identical: the stored value is the one this kernel would compute).

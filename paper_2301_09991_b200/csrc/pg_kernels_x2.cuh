@@ -294,8 +294,13 @@ constexpr size_t pg_k_x2_smem() {
             (size_t)(L + 2) * 2 * X2_KT * X2_CC) * sizeof(float);
 }
 
+// resident CTAs per SM of the fused diffusivity kernel: at p = 1 it fits 64 registers
+// (2 CTAs/SM; C3 K2 0.46 -> 0.40 ms, C5-weak 21.9 -> 18.5 ms), above that it keeps 1
+#ifndef CSN_K2F_MINB1
+#define CSN_K2F_MINB1 2
+#endif
 template <int L, bool EMA, int VEC>
-__global__ void __launch_bounds__(32 * X2_KT, 1)
+__global__ void __launch_bounds__(32 * X2_KT, L == 1 ? CSN_K2F_MINB1 : 1)
 pg_diffusivity_x2_kernel(const PGKArgs<float> a) {
     using TP = UnitTaps<L>;
     constexpr int KT = X2_KT;

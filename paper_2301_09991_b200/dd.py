@@ -34,8 +34,8 @@ from .eigen import Solver, SolverOptions, TransportSetup, setup_transport, _buff
 from .filters import build_upwind_filters
 from .grid import GridSpec
 from .materials import MaterialField
-from .multigrid import (CycleEngine, Level, MultigridHierarchy, UP_MAX_SWEEPS, _smooth_chain,
-                        build_hierarchy, coarsen_sigma, max_levels)
+from .multigrid import (CycleEngine, Level, MultigridHierarchy, UP_MAX_SWEEPS, XWindow,
+                        _FullWindow, _smooth_chain, build_hierarchy, coarsen_sigma, max_levels)
 from .quadrature import coarsen_quadrature
 
 GX = 5   # x-ghost columns of sources / corrections: the smoother's 3-sweep warm-up and
@@ -284,6 +284,11 @@ class DDCycleEngine(CycleEngine):
         self.src = [g.view for g in self.src_g]
         self.delta = [g.view for g in self.delta_g]
         self.use_graphs = False      # host barriers / NCCL calls between launches
+        # overlap: the PG kernels reading exchanged psi rows (K2, K3 / K3E, the fused
+        # sweep) are launched on the slab's interior columns while the exchange is in
+        # flight and on the edge columns after it (XWindow); CSN_DD_OVERLAP=0 waits for
+        # the exchange first and launches once (results are bit-identical either way)
+        self.overlap = os.environ.get("CSN_DD_OVERLAP", "1") != "0"
         cl = coarse_h.levels[0]
         self.coarse_eng = coarse_h.engine(n_group, dtype, device)
         # The gathered coarse solve and the local restriction chain are many short,
@@ -329,6 +334,31 @@ class DDCycleEngine(CycleEngine):
 
     def _hook_l1(self):
         self.comm.allreduce_sum_(self.l1)
+
+    def _hook_exchange_start(self, items):
+        h = self.h.levels[0].grid.halo
+        return self.comm.exchange_many([(t, w, h) for t, w in items])
+
+    def _windows(self, g, reach):
+        """Interior columns first (they read no ghost row, so they run while the exchange
+        is in flight), then — after the exchange — the edge columns beside each
+        neighbour.  The interior keeps `reach` columns plus one CTA tile's overhang away
+        from a ghosted side, rounded to the 8-column tile."""
+        full = [(_FullWindow(self.geoms[0]), True)]
+        if not self.overlap:
+            return full
+        gm = self.geoms[0]
+        e = 8 * ((reach + 7 + 7) // 8)
+        lo = e if gm.ghost_w else 0
+        hi = gm.nx - e if gm.ghost_e else gm.nx
+        if hi - lo < 8 or not (gm.ghost_w or gm.ghost_e):
+            return full
+        wins = [(XWindow(gm, lo, hi), False)]
+        if gm.ghost_w:
+            wins.append((XWindow(gm, 0, lo), True))
+        if gm.ghost_e:
+            wins.append((XWindow(gm, hi, gm.nx), True))
+        return wins
 
     def correction(self, r0, n_sweeps, finest_scale, out0=None, out0_halo=0, fold=False):
         if n_sweeps > UP_MAX_SWEEPS:

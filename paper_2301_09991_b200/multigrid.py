@@ -418,6 +418,54 @@ class PGState:
 GRAPH_MAX_DOF = 64 * 1024 * 1024
 
 
+class _NoWait:
+    def wait(self):
+        pass
+
+
+class XWindow:
+    """Columns [x0, x1) of a slab as a launch geometry of their own.
+
+    x is the slowest storage axis, so a window of any field is a narrowed view (a base
+    pointer offset); a cut side is flagged ghost in the window's ``csn_geom``, so the
+    kernels read the neighbouring columns of the same array there exactly as they read
+    exchanged halo rows at a rank boundary.  Per-cell arithmetic does not depend on the
+    tiling, so a field computed window by window is bit-identical to one launch.  Used
+    by the domain-decomposed engine to run the interior columns of the PG kernels while
+    the halo exchange is in flight and the edge columns after it (dd.py).
+    """
+
+    def __init__(self, gm, x0, x1):
+        self.x0, self.x1 = int(x0), int(x1)
+        self.gm = type(gm).from_buffer_copy(gm)
+        self.gm.nx = self.x1 - self.x0
+        if self.x0 > 0:
+            self.gm.ghost_w = 1
+        if self.x1 < gm.nx:
+            self.gm.ghost_e = 1
+
+    def pad(self, t, h):
+        """Window of a field padded by h: rows [x0, x1 + 2h) of the padded array."""
+        return None if t is None else t.narrow(0, self.x0, self.x1 - self.x0 + 2 * h)
+
+    def cells(self, t):
+        """Window of an unpadded per-cell array."""
+        return None if t is None else t.narrow(0, self.x0, self.x1 - self.x0)
+
+
+class _FullWindow:
+    """The whole slab (no narrowing): what the single-domain engine launches on."""
+
+    def __init__(self, gm):
+        self.gm = gm
+
+    def pad(self, t, h):
+        return t
+
+    def cells(self, t):
+        return t
+
+
 class CycleEngine:
     """Device workspaces + kernel sequence of one sawtooth cycle on one hierarchy."""
 
@@ -441,6 +489,7 @@ class CycleEngine:
         nparts = max(lib.csn_partials_size(_lib.dtype_code(self.r0), g, 3) for g in self.geoms)
         self.partials = torch.empty(int(nparts), dtype=torch.float64, device=device)
         self.l1 = torch.zeros(1, dtype=torch.float64, device=device)
+        self.l1w = None            # per-window L1 of a windowed residual (DD overlap)
         self.res_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
         self.psi_alt = None
         self.k_scratch = None
@@ -537,6 +586,17 @@ class CycleEngine:
 
     def _hook_l1(self):
         pass
+
+    def _hook_exchange_start(self, items):
+        """Start the ghost-row exchange of [(tensor, width)]; the returned handle's
+        wait() orders later launches after it.  Single domain: nothing to move."""
+        self._hook_exchange_many(items)
+        return _NoWait()
+
+    def _windows(self, g, reach):
+        """[(window, wait_first)] the PG kernels of one stage are launched on, in order:
+        the whole slab here; interior then edge columns on overlapping DD ranks."""
+        return [(_FullWindow(self.geoms[0]), True)]
 
     # ---------------------------------------------------------------- cycle
     def cycle(self, psi, q, fs=None, cfg=None, scheme="pg", n_sweeps=3, pg_sweeps=1,
@@ -722,35 +782,58 @@ class CycleEngine:
         if scheme == "pg" and plan["k2"] is not None and plan["k2"][0] is not None:
             avg_x = plan["k2"][0]
         # psi (and the averaged iterate before a live refresh) ghosts in one exchange
-        self._hook_exchange_many([(psi_in, reach)] + ([(avg_x, reach)] if avg_x is not None
-                                                       else []))
+        exch = self._hook_exchange_start([(psi_in, reach)] + ([(avg_x, reach)]
+                                                               if avg_x is not None else []))
         if scheme == "pg":
             kx, ky = plan["kx"], plan["ky"]
-            if plan["k2"] is not None:
-                avg_in, avg_out, mode, theta = plan["k2"]
-                nv = _Nvtx("csn.k_refresh")
+            h = g.halo
+            if plan["k2"] is not None and (self.k_work is None or
+                                           self.k_work[0] != (fs.order, psi_in.dtype)):
+                # split K2 (two y-marches through a psi_x, psi_y workspace) from the
+                # quadratic filters up; at p = 1 the fused two-stage kernel recomputes
+                # only 2 of 16 stage-1 columns and runs 2 CTAs/SM, and skipping the
+                # 16 B/DOF workspace round trip wins (C3 K2 0.56 -> 0.40 ms, C5-weak
+                # 23.5 -> 18.5 ms); CSN_K2_SPLIT=0/1 forces either
+                split = os.environ.get("CSN_K2_SPLIT", "1" if fs.order >= 2 else "0") == "1"
+                self.k_work = ((fs.order, psi_in.dtype),
+                               diffusivities_workspace(psi_in, self.geoms[0], fs.order)
+                               if split else None)
+            wins = self._windows(g, reach)
+            if len(wins) > 1 and (self.l1w is None or self.l1w.numel() < len(wins)):
+                self.l1w = torch.zeros(4, dtype=torch.float64, device=psi_in.device)
+            ema = plan["ema"]
+            for i, (win, wait) in enumerate(wins):
+                if wait:
+                    exch.wait()
+                if plan["k2"] is not None:
+                    avg_in, avg_out, mode, theta = plan["k2"]
+                    nv = _Nvtx("csn.k_refresh")
+                    nv.__enter__()
+                    t = self._t0()
+                    diffusivities_into(win.pad(psi_in, h), g, nd, ng, na, fs, cfg, c0["mu"],
+                                       c0["nu"], win.pad(kx, h), win.pad(ky, h), h,
+                                       avg_in=win.pad(avg_in, h), avg_out=win.pad(avg_out, h),
+                                       avg_mode=mode, theta=theta, gm=win.gm, work=self.k_work[1])
+                    self._t1("pg_diffusivity", t)
+                    nv.__exit__()
+                nv = _Nvtx("csn.residual")
                 nv.__enter__()
                 t = self._t0()
-                if self.k_work is None or self.k_work[0] != (fs.order, psi_in.dtype):
-                    self.k_work = ((fs.order, psi_in.dtype),
-                                   diffusivities_workspace(psi_in, self.geoms[0], fs.order))
-                diffusivities_into(psi_in, g, nd, ng, na, fs, cfg, c0["mu"], c0["nu"], kx, ky,
-                                   g.halo, avg_in=avg_in, avg_out=avg_out, avg_mode=mode,
-                                   theta=theta, gm=self.geoms[0], work=self.k_work[1])
-                self._t1("pg_diffusivity", t)
+                view.data = win.pad(psi_in, h)
+                pg_residual_launch(view, None, None, f.quad, fs, win.pad(kx, h), win.pad(ky, h), h,
+                                   r=win.cells(self.r0), r_halo=0, partials=self.partials,
+                                   l1=self.l1 if len(wins) == 1 else self.l1w[i:i + 1],
+                                   sigma=win.cells(self.sigma[0]), qt=win.cells(qt),
+                                   per_dof=per_dof, consts=c0, avg=win.pad(ema[0], h),
+                                   avg_mode=ema[1], theta=ema[2], gm=win.gm, dterm=self.dterm,
+                                   dterm_mode=plan["kd3"])
+                self._t1("pg_residual" if ema[1] == 0 else "pg_residual+ema", t)
                 nv.__exit__()
-            ema = plan["ema"]
-            nv = _Nvtx("csn.residual")
-            nv.__enter__()
-            t = self._t0()
-            pg_residual_launch(view, None, None, f.quad, fs, kx, ky, g.halo, r=self.r0, r_halo=0,
-                               partials=self.partials, l1=self.l1, sigma=self.sigma[0], qt=qt,
-                               per_dof=per_dof, consts=c0, avg=ema[0], avg_mode=ema[1],
-                               theta=ema[2], gm=self.geoms[0], dterm=self.dterm,
-                               dterm_mode=plan["kd3"])
-            self._t1("pg_residual" if ema[1] == 0 else "pg_residual+ema", t)
-            nv.__exit__()
+            view.data = psi_in
+            if len(wins) > 1:      # fixed-order fp64 sum of the windows' L1
+                torch.sum(self.l1w[:len(wins)], dim=0, keepdim=True, out=self.l1)
         else:
+            exch.wait()
             t = self._t0()
             _lib.call("csn_upwind_residual", dt, self.geoms[0], _lib.ptr(psi_in), g.halo,
                       _lib.ptr(self.sigma[0]), _lib.ptr(qt), per_dof, _lib.ptr(c0["mu"]),
@@ -783,13 +866,15 @@ class CycleEngine:
         nv = _Nvtx("csn.correction")
         nv.__enter__()
         t = self._t0()
+        exch = _NoWait()
         if fold:
             # psi' = psi - delta in place, then its boundary (R/multigrid.py:301, :166)
             self.correction(self.r0, n_sweeps, cfg.beta_diag, psi_in, g.halo, fold=True)
             _lib.call("csn_apply_boundary", dt, self.geoms[0], _lib.ptr(psi_in), g.halo,
                       _lib.ptr(c0["mu"]), _lib.ptr(c0["nu"]), _lib.stream())
-            # DD ranks: psi' ghost rows for the sweep's l-wide x reach
-            self._hook_exchange_many([(psi_in, fs.half_width)])
+            # DD ranks: psi' ghost rows for the sweep's l-wide x reach (in flight while
+            # the sweep's interior columns run)
+            exch = self._hook_exchange_start([(psi_in, fs.half_width)])
             delta = None
         else:
             delta = self.correction(self.r0, n_sweeps, cfg.beta_diag if scheme == "pg" else 1.0,
@@ -813,12 +898,21 @@ class CycleEngine:
                               g.halo, _lib.ptr(c0["mu"]), _lib.ptr(c0["nu"]), _lib.stream())
                     self._hook_exchange_many([(bufs[k % 2], fs.half_width)])
                 t = self._t0()
-                pg_residual_launch(view, None, None, f.quad, fs, plan["kx"], plan["ky"], g.halo,
-                                   psi_out=bufs[(k + 1) % 2], out_halo=g.halo,
-                                   delta=delta if k == 0 else None, delta_halo=dh,
-                                   beta=cfg.beta_diag, sigma=self.sigma[0], qt=qt,
-                                   per_dof=per_dof, consts=c0, gm=self.geoms[0],
-                                   dterm=self.dterm, dterm_mode=plan["kd5"] if k == 0 else 0)
+                h = g.halo
+                # the folded first sweep may run window by window around the exchange
+                wins = (self._windows(g, fs.half_width) if k == 0 and fold
+                        else [(_FullWindow(self.geoms[0]), True)])
+                for win, wait in wins:
+                    if wait:
+                        exch.wait()
+                    view.data = win.pad(bufs[k % 2], h)
+                    pg_residual_launch(view, None, None, f.quad, fs, win.pad(plan["kx"], h),
+                                       win.pad(plan["ky"], h), h,
+                                       psi_out=win.pad(bufs[(k + 1) % 2], h), out_halo=h,
+                                       delta=delta if k == 0 else None, delta_halo=dh,
+                                       beta=cfg.beta_diag, sigma=win.cells(self.sigma[0]),
+                                       qt=win.cells(qt), per_dof=per_dof, consts=c0, gm=win.gm,
+                                       dterm=self.dterm, dterm_mode=plan["kd5"] if k == 0 else 0)
                 self._t1("pg_sweep", t)
             view.data = bufs[plan["pg_sweeps"] % 2]
         else:

@@ -117,6 +117,29 @@ def test_dd_ragged_slab_and_pg_sweeps(case, dtype, size):
         assert r.pg_log == ref.pg_log
 
 
+@pytest.mark.parametrize("case,size", [("c4", 2), ("c4", 4), ("c3", 2), ("c2", 2)])
+def test_dd_overlap_windows_bitwise(case, size, monkeypatch):
+    """The PG kernels launched on interior columns while the exchange is in flight and on
+    edge columns after it (XWindow, CSN_DD_OVERLAP=1, the default) give the flux of the
+    one-launch path bit for bit; only the fp64 L1 is summed in window order."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_2301_09991_b200 as P
+    from paper_2301_09991_b200 import benchmarks as B
+    pd = {"c4": lambda: B.c4(nx=256, blocks=4, n_a=8, cycles=6),
+          "c2": lambda: B.c2(nx=128, blocks=8, n_a=8, cycles=6),
+          "c3": lambda: B.c3(n_pins=4, cells_per_pin=32, n_a=8, outers=2, inner=3)}[case]()
+    opts = _opts(P, pd, "float32")
+    monkeypatch.setenv("CSN_DD_OVERLAP", "0")
+    off = _run_dd(pd, opts, size)
+    monkeypatch.setenv("CSN_DD_OVERLAP", "1")
+    on = _run_dd(pd, opts, size)
+    for a, b in zip(on, off):
+        assert np.array_equal(a.phi, b.phi)
+        np.testing.assert_allclose(a.residual_history, b.residual_history, rtol=1e-13)
+        assert a.pg_log == b.pg_log
+
+
 def test_dd_rejects_narrow_slabs():
     """A slab narrower than the widest halo exchange (3l psi rows on live cycles) is
     refused instead of sending the sender's own ghost rows."""
