@@ -109,6 +109,22 @@ inline int grid1d(int64_t n, int block = 256) {
 // grid still holds >= 8 CTAs per SM
 inline int up_chunks0(int nx) { return (int)cdiv(nx, 8); }
 
+// x chunks of one smoother launch over `ctas_xy` (strip x channel) CTAs: 8-column chunks
+// merged while the grid keeps >= 8 CTAs per SM; a grid below one wave (the coarse levels)
+// is instead split down to single columns while it still fits one wave — a chunk's march
+// is a serial chain of (columns + H warm-up) dependent steps of ~1.5 us each with one warp
+// per SM, so a 16 x 16 level took 16 us as one 8-column chunk (11 steps) and takes 4
+// steps as single columns (the 4x warm-up recompute is free at that size)
+// (min_cols: the packed kernels start a non-first chunk's warm-up H columns before it
+// without an x predicate, so their chunks keep >= 4 columns; the scalar kernel
+// predicates every column)
+inline int up_chunks(int nx, int64_t ctas_xy, int min_cols) {
+    int chunks = up_chunks0(nx);
+    while (chunks > 1 && ctas_xy * (chunks / 2) >= 148 * 8) chunks /= 2;
+    while (cdiv(nx, chunks * 2) >= min_cols && ctas_xy * chunks * 2 <= 148 * 2) chunks *= 2;
+    return chunks;
+}
+
 // rows per CTA chunk for the y-marching kernels: enough CTAs to fill 148 SMs ~4x
 inline int pick_ly(int64_t ctas_xy, int rows, int T) {
     int chunks = 1;
@@ -448,8 +464,7 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
             !(g1 && init_mode == 2 && !a.angle_coarsens)) {
             const int gx = (int)cdiv(cdiv(g->ny, UPX_UT), UPX_SPB);
             const int gy = (int)(C / UPX_CC);
-            int chunks = up_chunks0(g->nx);
-            while (chunks > 1 && (int64_t)gx * gy * (chunks / 2) >= 148 * 8) chunks /= 2;
+            const int chunks = up_chunks(g->nx, (int64_t)gx * gy, 4);
             a.xchunk = (int)cdiv(g->nx, chunks);
             const int gz = (int)cdiv(g->nx, a.xchunk);
             dim3 grid(gx, gy, gz), block(32, UPX_SPB);
@@ -515,8 +530,7 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
             C % UPX1_CC == 0 && face % UPX1_CC == 0) {
             const int gx = (int)cdiv(cdiv(g->ny, UPX_UT), UPX_SPB);
             const int gy = (int)(C / UPX1_CC);
-            int chunks = up_chunks0(g->nx);
-            while (chunks > 1 && (int64_t)gx * gy * (chunks / 2) >= 148 * 8) chunks /= 2;
+            const int chunks = up_chunks(g->nx, (int64_t)gx * gy, 4);
             a.xchunk = (int)cdiv(g->nx, chunks);
             const int gz = (int)cdiv(g->nx, a.xchunk);
             upwind_smooth_x1_kernel<3><<<dim3(gx, gy, gz), dim3(32, UPX_SPB), 0, st>>>(a);
@@ -527,8 +541,7 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
     const int gx = (int)cdiv(cdiv(g->ny, UT), UP_SPB);
     const int gy = (int)cdiv((int64_t)g->nd * g->ng, UP_CC);
     // x chunks: keep chunks long against the H-column warm-up, fill the machine
-    int chunks = up_chunks0(g->nx);
-    while (chunks > 1 && (int64_t)gx * gy * (chunks / 2) >= 148 * 8) chunks /= 2;
+    const int chunks = up_chunks(g->nx, (int64_t)gx * gy, 1);
     a.xchunk = (int)cdiv(g->nx, chunks);
     const int gz = (int)cdiv(g->nx, a.xchunk);
     dim3 grid(gx, gy, gz), block(UP_CC, UP_SPB);

@@ -289,6 +289,7 @@ class DDCycleEngine(CycleEngine):
         # flight and on the edge columns after it (XWindow); CSN_DD_OVERLAP=0 waits for
         # the exchange first and launches once (results are bit-identical either way)
         self.overlap = os.environ.get("CSN_DD_OVERLAP", "1") != "0"
+        self.overlap_min_bytes = int(os.environ.get("CSN_DD_OVERLAP_MIN_MB", "32")) << 20
         cl = coarse_h.levels[0]
         self.coarse_eng = coarse_h.engine(n_group, dtype, device)
         # The gathered coarse solve and the local restriction chain are many short,
@@ -339,25 +340,31 @@ class DDCycleEngine(CycleEngine):
         h = self.h.levels[0].grid.halo
         return self.comm.exchange_many([(t, w, h) for t, w in items])
 
-    def _windows(self, g, reach):
-        """Interior columns first (they read no ghost row, so they run while the exchange
-        is in flight), then — after the exchange — the edge columns beside each
-        neighbour.  The interior keeps `reach` columns plus one CTA tile's overhang away
-        from a ghosted side, rounded to the 8-column tile."""
-        full = [(_FullWindow(self.geoms[0]), True)]
-        if not self.overlap:
-            return full
+    def _windows(self, g, reach, n_fields=1):
+        """The interior columns (they read no ghost row, so they run while the exchange is
+        in flight) and the edge columns beside each neighbour (after the exchange, on the
+        side stream).  The interior keeps `reach` columns plus one CTA tile's overhang
+        away from a ghosted side, rounded to the 8-column tile.  Only exchanges of at least
+        ``overlap_min_bytes`` per side are overlapped: the windowed launches cost ~0.1 ms
+        per cycle on a 64-column C4 slab (tools/dd_rank_cost.py), which the 3l-row psi +
+        averaged-iterate bands of a live cycle (78 MB per side at 8 ranks) repay and the
+        l-row bands of frozen cycles and of the sweep (13 MB) do not."""
+        full = [_FullWindow(self.geoms[0])]
         gm = self.geoms[0]
+        h = self.h.levels[0].grid.halo
+        band = reach * (gm.ny + 2 * h) * gm.nd * gm.ng * self.r0.element_size() * n_fields
+        if not self.overlap or band < self.overlap_min_bytes:
+            return full
         e = 8 * ((reach + 7 + 7) // 8)
         lo = e if gm.ghost_w else 0
         hi = gm.nx - e if gm.ghost_e else gm.nx
         if hi - lo < 8 or not (gm.ghost_w or gm.ghost_e):
             return full
-        wins = [(XWindow(gm, lo, hi), False)]
+        wins = [XWindow(gm, lo, hi)]
         if gm.ghost_w:
-            wins.append((XWindow(gm, 0, lo), True))
+            wins.append(XWindow(gm, 0, lo, edge=True))
         if gm.ghost_e:
-            wins.append((XWindow(gm, hi, gm.nx), True))
+            wins.append(XWindow(gm, hi, gm.nx, edge=True))
         return wins
 
     def correction(self, r0, n_sweeps, finest_scale, out0=None, out0_halo=0, fold=False):

@@ -435,8 +435,9 @@ class XWindow:
     the halo exchange is in flight and the edge columns after it (dd.py).
     """
 
-    def __init__(self, gm, x0, x1):
+    def __init__(self, gm, x0, x1, edge=False):
         self.x0, self.x1 = int(x0), int(x1)
+        self.edge = edge           # reads exchanged ghost rows (runs after the exchange)
         self.gm = type(gm).from_buffer_copy(gm)
         self.gm.nx = self.x1 - self.x0
         if self.x0 > 0:
@@ -455,6 +456,8 @@ class XWindow:
 
 class _FullWindow:
     """The whole slab (no narrowing): what the single-domain engine launches on."""
+
+    edge = False
 
     def __init__(self, gm):
         self.gm = gm
@@ -490,6 +493,9 @@ class CycleEngine:
         self.partials = torch.empty(int(nparts), dtype=torch.float64, device=device)
         self.l1 = torch.zeros(1, dtype=torch.float64, device=device)
         self.l1w = None            # per-window L1 of a windowed residual (DD overlap)
+        self._side_stream = None   # edge windows run here beside the interior
+        self._npart = int(nparts)
+        self.k_work_edge = None    # (key, split-K2 workspace of the edge windows)
         self.res_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
         self.psi_alt = None
         self.k_scratch = None
@@ -593,10 +599,37 @@ class CycleEngine:
         self._hook_exchange_many(items)
         return _NoWait()
 
-    def _windows(self, g, reach):
-        """[(window, wait_first)] the PG kernels of one stage are launched on, in order:
-        the whole slab here; interior then edge columns on overlapping DD ranks."""
-        return [(_FullWindow(self.geoms[0]), True)]
+    def _windows(self, g, reach, n_fields=1):
+        """Windows the PG kernels of one stage are launched on: the whole slab here; on
+        overlapping DD ranks the interior columns first (they read no exchanged row) and
+        the edge columns beside each neighbour (``edge = True``: after the exchange)."""
+        return [_FullWindow(self.geoms[0])]
+
+    def _run_windows(self, wins, exch, run):
+        """run(i, window) for every window.  One window: after the exchange, on the
+        current stream.  Interior + edges: the interior runs on the current stream while
+        the exchange is in flight; the edge windows wait for the exchange on a side
+        stream and run beside the interior (their CTAs fill the machine as the interior
+        drains, where a launch of their own would leave most of a wave idle); the current
+        stream then joins the side stream."""
+        if len(wins) == 1:
+            exch.wait()
+            run(0, wins[0])
+            return
+        main = torch.cuda.current_stream()
+        if self._side_stream is None:
+            self._side_stream = torch.cuda.Stream(device=self.device)
+        side = self._side_stream
+        side.wait_stream(main)
+        for i, w in enumerate(wins):
+            if not w.edge:
+                run(i, w)
+        with torch.cuda.stream(side):
+            exch.wait()
+            for i, w in enumerate(wins):
+                if w.edge:
+                    run(i, w)
+        main.wait_stream(side)
 
     # ---------------------------------------------------------------- cycle
     def cycle(self, psi, q, fs=None, cfg=None, scheme="pg", n_sweeps=3, pg_sweeps=1,
@@ -798,13 +831,24 @@ class CycleEngine:
                 self.k_work = ((fs.order, psi_in.dtype),
                                diffusivities_workspace(psi_in, self.geoms[0], fs.order)
                                if split else None)
-            wins = self._windows(g, reach)
-            if len(wins) > 1 and (self.l1w is None or self.l1w.numel() < len(wins)):
+            wins = self._windows(g, reach, 2 if avg_x is not None else 1)
+            multi = len(wins) > 1
+            if multi and self.l1w is None:
                 self.l1w = torch.zeros(4, dtype=torch.float64, device=psi_in.device)
+                # windows on two streams: one block of reduction partials per window
+                self.partials = torch.empty(4 * self._npart, dtype=torch.float64,
+                                            device=psi_in.device)
+            work_e = None
+            if multi and plan["k2"] is not None and self.k_work[1] is not None:
+                ew = max(w.x1 - w.x0 for w in wins if w.edge)
+                key = (fs.order, psi_in.dtype, ew)
+                if self.k_work_edge is None or self.k_work_edge[0] != key:
+                    ge = XWindow(self.geoms[0], 0, ew).gm
+                    self.k_work_edge = (key, diffusivities_workspace(psi_in, ge, fs.order))
+                work_e = self.k_work_edge[1]
             ema = plan["ema"]
-            for i, (win, wait) in enumerate(wins):
-                if wait:
-                    exch.wait()
+
+            def run(i, win):
                 if plan["k2"] is not None:
                     avg_in, avg_out, mode, theta = plan["k2"]
                     nv = _Nvtx("csn.k_refresh")
@@ -813,24 +857,30 @@ class CycleEngine:
                     diffusivities_into(win.pad(psi_in, h), g, nd, ng, na, fs, cfg, c0["mu"],
                                        c0["nu"], win.pad(kx, h), win.pad(ky, h), h,
                                        avg_in=win.pad(avg_in, h), avg_out=win.pad(avg_out, h),
-                                       avg_mode=mode, theta=theta, gm=win.gm, work=self.k_work[1])
+                                       avg_mode=mode, theta=theta, gm=win.gm,
+                                       work=work_e if win.edge else self.k_work[1])
                     self._t1("pg_diffusivity", t)
                     nv.__exit__()
                 nv = _Nvtx("csn.residual")
                 nv.__enter__()
                 t = self._t0()
-                view.data = win.pad(psi_in, h)
-                pg_residual_launch(view, None, None, f.quad, fs, win.pad(kx, h), win.pad(ky, h), h,
-                                   r=win.cells(self.r0), r_halo=0, partials=self.partials,
-                                   l1=self.l1 if len(wins) == 1 else self.l1w[i:i + 1],
+                v = Field.__new__(Field)
+                v.grid = g
+                v.data = win.pad(psi_in, h)
+                pg_residual_launch(v, None, None, f.quad, fs, win.pad(kx, h), win.pad(ky, h), h,
+                                   r=win.cells(self.r0), r_halo=0,
+                                   partials=self.partials[i * self._npart:] if multi
+                                   else self.partials,
+                                   l1=self.l1w[i:i + 1] if multi else self.l1,
                                    sigma=win.cells(self.sigma[0]), qt=win.cells(qt),
                                    per_dof=per_dof, consts=c0, avg=win.pad(ema[0], h),
                                    avg_mode=ema[1], theta=ema[2], gm=win.gm, dterm=self.dterm,
                                    dterm_mode=plan["kd3"])
                 self._t1("pg_residual" if ema[1] == 0 else "pg_residual+ema", t)
                 nv.__exit__()
-            view.data = psi_in
-            if len(wins) > 1:      # fixed-order fp64 sum of the windows' L1
+
+            self._run_windows(wins, exch, run)
+            if multi:              # fixed-order fp64 sum of the windows' L1
                 torch.sum(self.l1w[:len(wins)], dim=0, keepdim=True, out=self.l1)
         else:
             exch.wait()
@@ -901,18 +951,22 @@ class CycleEngine:
                 h = g.halo
                 # the folded first sweep may run window by window around the exchange
                 wins = (self._windows(g, fs.half_width) if k == 0 and fold
-                        else [(_FullWindow(self.geoms[0]), True)])
-                for win, wait in wins:
-                    if wait:
-                        exch.wait()
-                    view.data = win.pad(bufs[k % 2], h)
-                    pg_residual_launch(view, None, None, f.quad, fs, win.pad(plan["kx"], h),
+                        else [_FullWindow(self.geoms[0])])
+
+                def run(i, win, k=k):
+                    v = Field.__new__(Field)
+                    v.grid = g
+                    v.data = win.pad(bufs[k % 2], h)
+                    pg_residual_launch(v, None, None, f.quad, fs, win.pad(plan["kx"], h),
                                        win.pad(plan["ky"], h), h,
                                        psi_out=win.pad(bufs[(k + 1) % 2], h), out_halo=h,
                                        delta=delta if k == 0 else None, delta_halo=dh,
                                        beta=cfg.beta_diag, sigma=win.cells(self.sigma[0]),
                                        qt=win.cells(qt), per_dof=per_dof, consts=c0, gm=win.gm,
                                        dterm=self.dterm, dterm_mode=plan["kd5"] if k == 0 else 0)
+
+                self._run_windows(wins, exch, run)
+                exch = _NoWait()
                 self._t1("pg_sweep", t)
             view.data = bufs[plan["pg_sweeps"] % 2]
         else:

@@ -12,6 +12,13 @@ from conftest import rel_l2
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _overlap_every_exchange(monkeypatch):
+    """Window every exchanged stage (the default only overlaps bands >= 32 MB per side), so
+    the small test slabs exercise the interior / edge launches of K2, K3, K3E and the sweep."""
+    monkeypatch.setenv("CSN_DD_OVERLAP_MIN_MB", "0")
+
+
 def _opts(P, pd, dtype):
     o = dict(pd.options)
     pg = o.pop("pg", None)
