@@ -132,6 +132,24 @@ int csn_restrict(int dtype, const csn_geom* gf, const csn_geom* gc,
                  const void* fine, int fine_halo, const void* w_f, const void* w_c,
                  int normalise, void* coarse, int coarse_halo, void* stream);
 
+/* R/multigrid.py:309-339 mg_correction on the coarse tail of the hierarchy, one launch:
+ * n levels (finest first; level i + 1 is the spatial 2:1 / angular 1:1 or 2:1 coarsening
+ * of level i, no ghost sides), each at most CSN_TAIL_MAX_DOF degrees of freedom.
+ *   src[0] (given) is restricted and normalised down the chain into src[1..n-1]
+ *   (R/multigrid.py:318-326); then from the coarsest level up each delta[i] is n_sweeps
+ *   upwind Jacobi sweeps (diag_scale 1) on src[i] starting from the prolongation of
+ *   delta[i + 1] (zero on the coarsest) (R/multigrid.py:330-338).
+ * geoms: host array of n csn_geom; sigma/mu/nu/strm/w/src/delta: HOST arrays of n device
+ * pointers (sigma [nx][ny][ng]; mu, nu, strm, w [nd]; src, delta unpadded [nx][ny][nd][ng]);
+ * scratch: device buffer of >= the largest level's DOF (field dtype).
+ * fp32 results are bit-identical to csn_restrict + csn_upwind_smooth level by level. */
+#define CSN_TAIL_MAX_LEVELS 12
+#define CSN_TAIL_MAX_DOF 32768
+int csn_coarse_tail(int dtype, int n, const csn_geom* geoms, const void* const* sigma,
+                    const void* const* mu, const void* const* nu, const void* const* strm,
+                    const void* const* w, void* const* src, void* const* delta, void* scratch,
+                    int n_sweeps, void* stream);
+
 /* R/multigrid.py:130-146 prolong (piecewise-constant injection). */
 int csn_prolong(int dtype, const csn_geom* gc, const csn_geom* gf,
                 const void* coarse, int coarse_halo, void* fine, int fine_halo,

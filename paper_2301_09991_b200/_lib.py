@@ -43,6 +43,8 @@ _SIGNATURES = {
     "csn_upwind_smooth_sub": ([_c_int, _GP, _vp, _c_int, _c_int, _vp, _c_int, _GP, _vp, _vp, _vp,
                                _vp, _c_int, _c_dbl, _vp, _c_int, _vp], _c_int),
     "csn_restrict": ([_c_int, _GP, _GP, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _vp], _c_int),
+    "csn_coarse_tail": ([_c_int, _c_int, _GP, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _vp],
+                        _c_int),
     "csn_prolong": ([_c_int, _GP, _GP, _vp, _c_int, _vp, _c_int, _vp], _c_int),
     "csn_pg_diffusivities": ([_c_int, _c_int, _GP, _DP, _DP, _vp, _c_int, _vp, _c_int, _vp, _c_int,
                               _c_int, _c_dbl, _vp, _vp, _vp, _vp, _c_int, _vp, _vp], _c_int),

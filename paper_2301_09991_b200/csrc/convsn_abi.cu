@@ -11,6 +11,7 @@
 #include "pg_kernels_x2.cuh"
 #include "upwind_kernels.cuh"
 #include "pg_kernels_tma.cuh"
+#include "tail_kernels.cuh"
 #include "launchers.h"
 
 // NVTX ranges around every compute entry point (header-only nvtx3: a no-op function
@@ -748,6 +749,65 @@ int csn_restrict(int dtype, const csn_geom* gf, const csn_geom* gc, const void* 
         if (gyc < 1) gyc = 1;
         restrict_kernel<Real><<<dim3((unsigned)gxc, (unsigned)gyc), 256, 0, S(stream)>>>(a);
         CSN_CHECK_LAUNCH();
+        return CSN_OK;
+    };
+    if (dtype == CSN_F32) return run(float());
+    if (dtype == CSN_F64) return run(double());
+    return CSN_E_DTYPE;
+}
+
+int csn_coarse_tail(int dtype, int n, const csn_geom* geoms, const void* const* sigma,
+                    const void* const* mu, const void* const* nu, const void* const* strm,
+                    const void* const* w, void* const* src, void* const* delta, void* scratch,
+                    int n_sweeps, void* stream) {
+    CSN_NVTX();
+    if (n < 1 || n > TAIL_MAX_LEVELS || !geoms || !sigma || !mu || !nu || !strm || !w || !src ||
+        !delta || !scratch || n_sweeps < 0)
+        return CSN_E_ARG;
+    for (int i = 0; i < n; ++i) {
+        const csn_geom& g = geoms[i];
+        if (!geom_ok(&g) || g.ghost_w || g.ghost_e || !sigma[i] || !mu[i] || !nu[i] || !strm[i] ||
+            !w[i] || !src[i] || !delta[i])
+            return CSN_E_ARG;
+        if ((int64_t)g.nx * g.ny * g.nd * g.ng > CSN_TAIL_MAX_DOF) return CSN_E_ARG;
+        if (i > 0) {
+            const csn_geom& f = geoms[i - 1];
+            if (g.nx * 2 != f.nx || g.ny * 2 != f.ny || g.ng != f.ng ||
+                (g.na != f.na && g.na * 2 != f.na))
+                return CSN_E_ARG;
+        }
+    }
+    auto run = [&](auto tag) -> int {
+        using Real = decltype(tag);
+        TailArgs<Real> t;
+        t.n = n;
+        for (int i = 0; i < n; ++i) {
+            TailLevel<Real>& L = t.lv[i];
+            L.g = make_geo(geoms[i]);
+            L.sigma = (const Real*)sigma[i];
+            L.mu = (const Real*)mu[i]; L.nu = (const Real*)nu[i];
+            L.strm = (const Real*)strm[i]; L.w = (const Real*)w[i];
+            L.src = (Real*)src[i]; L.delta = (Real*)delta[i];
+            L.inv_dx = (Real)(1.0 / geoms[i].dx); L.inv_dy = (Real)(1.0 / geoms[i].dy);
+            L.area = (Real)(geoms[i].dx * geoms[i].dy);
+        }
+        t.scratch = (Real*)scratch;
+        t.n_sweeps = n_sweeps;
+        t.exact_div = std::is_same<Real, float>::value ? g_tune_upwind_div : 0;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(TAIL_CTAS);
+        cfg.blockDim = dim3(TAIL_THREADS);
+        cfg.stream = S(stream);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = TAIL_CTAS;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, coarse_tail_kernel<Real>, t);
+        if (e != cudaSuccess) return -(int)e;
+        ++g_launches;
         return CSN_OK;
     };
     if (dtype == CSN_F32) return run(float());

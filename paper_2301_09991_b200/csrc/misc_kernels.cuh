@@ -32,11 +32,11 @@ struct RestrictArgs {
 // cells with blockIdx.y: the channel decomposition (children, weights, normaliser) is
 // done once per thread, the cell loop is loads + the reference's arithmetic order.  With angle coarsening and
 // ng == 1 the two column children (pb = 0, 1) are adjacent channels: one 8-byte load.
+// (restrict_cells: coarse channel cc over the coarse cells cell0, cell0 + stride, ...)
 template <class Real>
-__global__ void __launch_bounds__(256) restrict_kernel(const RestrictArgs<Real> a) {
+__device__ __forceinline__ void restrict_cells(const RestrictArgs<Real>& a, const int cc,
+                                               const int cell0, const int stride) {
     const Geo &gf = a.gf, &gc = a.gc;
-    const int cc = blockIdx.x * blockDim.x + threadIdx.x;
-    if (cc >= gc.C) return;
     const int N = cc / gc.ng, g = cc - N * gc.ng;
     int cf[4];          // fine child channels (pa, pb) = (0,0), (0,1), (1,0), (1,1)
     Real wn[4];
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(256) restrict_kernel(const RestrictArgs<Real> 
     const bool pair = nch == 4 && gf.ng == 1;      // cf[1] == cf[0] + 1, cf[0] even
     const int64_t fpitch = (int64_t)(gf.ny + 2 * a.fine_h) * gf.C;   // x stride (fine)
     const int ncells = gc.nx * gc.ny;
-    for (int cell = blockIdx.y; cell < ncells; cell += gridDim.y) {
+    for (int cell = cell0; cell < ncells; cell += stride) {
         const int I = cell / gc.ny, J = cell - I * gc.ny;
         const Real* f0 = a.fine + fidx(2 * I, 2 * J, 0, gf.ny, a.fine_h, gf.C);
         Real acc = Real(0);
@@ -103,6 +103,13 @@ __global__ void __launch_bounds__(256) restrict_kernel(const RestrictArgs<Real> 
         if (a.normalise) acc = div_rn(acc, norm);
         a.coarse[fidx(I, J, cc, gc.ny, a.coarse_h, gc.C)] = acc;
     }
+}
+
+template <class Real>
+__global__ void __launch_bounds__(256) restrict_kernel(const RestrictArgs<Real> a) {
+    const int cc = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cc >= a.gc.C) return;
+    restrict_cells(a, cc, (int)blockIdx.y, (int)gridDim.y);
 }
 
 template <class Real>

@@ -11,9 +11,11 @@ hierarchy and issues the kernel sequence; the per-cycle host work is the fp64
 residual read-back that drives ``PGState``.
 """
 
+import ctypes
 import gc
 import itertools
 import os
+
 import numpy as np
 import torch
 
@@ -416,6 +418,8 @@ class PGState:
 
 
 GRAPH_MAX_DOF = 64 * 1024 * 1024
+TAIL_MAX_DOF = 32768       # CSN_TAIL_MAX_DOF (include/convsn_sm100.h)
+TAIL_MAX_LEVELS = 12
 
 
 class _NoWait:
@@ -493,6 +497,7 @@ class CycleEngine:
         self.partials = torch.empty(int(nparts), dtype=torch.float64, device=device)
         self.l1 = torch.zeros(1, dtype=torch.float64, device=device)
         self.l1w = None            # per-window L1 of a windowed residual (DD overlap)
+        self._tail_args = False    # coarse-tail argument block (built on first use)
         self._side_stream = None   # edge windows run here beside the interior
         self._npart = int(nparts)
         self.k_work_edge = None    # (key, split-K2 workspace of the edge windows)
@@ -558,12 +563,23 @@ class CycleEngine:
         L = self.h.levels
         dt = _lib.dtype_code(r0)
         src = [r0] + self.src[1:]
-        for i in range(1, len(L)):
+        tail = self._tail() if r0.dtype == self.dtype else None
+        n_res = len(L) if tail is None else tail["start"] + 1
+        for i in range(1, n_res):
             _lib.call("csn_restrict", dt, self.geoms[i - 1], self.geoms[i], _lib.ptr(src[i - 1]),
                       0, _lib.ptr(self.consts[i - 1]["w"]), _lib.ptr(self.consts[i]["w"]), 1,
                       _lib.ptr(src[i]), 0, _lib.stream())
         prev = None
-        for i in range(len(L) - 1, -1, -1):
+        top = len(L) - 1
+        if tail is not None:
+            # the coarse tail (every level of <= TAIL_MAX_DOF unknowns): its restriction
+            # chain and all its smoothing in one cluster launch (csrc/tail_kernels.cuh)
+            _lib.call("csn_coarse_tail", dt, tail["n"], tail["geoms"], tail["sigma"], tail["mu"],
+                      tail["nu"], tail["strm"], tail["w"], tail["src"], tail["delta"],
+                      _lib.ptr(tail["scratch"]), int(n_sweeps), _lib.stream())
+            prev = self.delta[tail["start"]]
+            top = tail["start"] - 1
+        for i in range(top, -1, -1):
             scale = finest_scale if i == 0 else 1.0
             if n_sweeps > UP_MAX_SWEEPS and self.spare[i] is None:
                 self.spare[i] = torch.empty_like(self.delta[i])
@@ -580,6 +596,37 @@ class CycleEngine:
             prev = _smooth_chain(L[i], self.ng, src[i], 1, init, mode, 0, gc, n_sweeps, scale,
                                  self.delta[i], 0, self.spare[i], self.sigma[i], self.geoms[i])
         return prev
+
+    def _tail(self):
+        """Argument block of the one-launch coarse tail: the levels from the first one
+        (>= 1) holding <= TAIL_MAX_DOF unknowns down to the coarsest; None when fewer than
+        two levels qualify or CSN_TAIL=0."""
+        if self._tail_args is not False:
+            return self._tail_args
+        self._tail_args = None
+        if os.environ.get("CSN_TAIL", "1") == "0":
+            return None
+        dof = [int(np.prod(s)) for s in self.shapes]
+        start = next((i for i in range(1, len(dof)) if dof[i] <= TAIL_MAX_DOF), None)
+        if start is None or len(dof) - start < 2 or len(dof) - start > TAIL_MAX_LEVELS:
+            return None
+        n = len(dof) - start
+        vp = ctypes.c_void_p * n
+        arr = lambda ts: vp(*[t.data_ptr() for t in ts])
+        lv = range(start, len(dof))
+        self._tail_args = {
+            "start": start, "n": n,
+            "geoms": (_lib.Geom * n)(*[self.geoms[i] for i in lv]),
+            "sigma": arr([self.sigma[i] for i in lv]),
+            "mu": arr([self.consts[i]["mu"] for i in lv]),
+            "nu": arr([self.consts[i]["nu"] for i in lv]),
+            "strm": arr([self.consts[i]["strm"] for i in lv]),
+            "w": arr([self.consts[i]["w"] for i in lv]),
+            "src": arr([self.src[i] for i in lv]),
+            "delta": arr([self.delta[i] for i in lv]),
+            "scratch": torch.empty(dof[start], dtype=self.dtype, device=self.device),
+        }
+        return self._tail_args
 
     # hooks for domain decomposition (dd.py): halo exchange / reductions; no-ops here
     def _hook_exchange(self, name, t, width):

@@ -153,6 +153,34 @@ def test_transfers_and_correction(P, na, ng, dt, tol):
     assert rel_l2(interior(host(delta.data), 1), interior(g[f"{key}_mgc"], 1)) < tol
 
 
+@pytest.mark.parametrize("na,ng,nx,ny", [(4, 1, 64, 64), (8, 2, 32, 64), (2, 7, 48, 16), (1, 1, 8, 8)])
+@pytest.mark.parametrize("sweeps", [3, 5, 0])
+@pytest.mark.parametrize("dt", [F32, F64])
+def test_coarse_tail_matches_levels(P, na, ng, nx, ny, sweeps, dt, monkeypatch):
+    """The one-launch coarse tail (csn_coarse_tail: restriction chain + every smoothing of
+    the levels with <= 32768 unknowns in one cluster launch, R/multigrid.py:309-339) against
+    csn_restrict + csn_upwind_smooth level by level: fp32 bit for bit (same rounded
+    operations), fp64 to rounding (the compiler contracts the two kernels' fp64
+    expressions independently)."""
+    q = P.build_quadrature(na)
+    grid = P.GridSpec(nx, ny, 0.25, 0.5, 1)
+    rng = np.random.default_rng(nx * 131 + ng)
+    sigma = rng.uniform(0.1, 8.0, size=(nx, ny, ng))
+    r = torch.as_tensor(rng.standard_normal((nx, ny, q.n_dir, ng)), dtype=dt, device="cuda")
+    out = {}
+    for tail in ("0", "1"):
+        monkeypatch.setenv("CSN_TAIL", tail)
+        hier = P.build_hierarchy(grid, q, sigma)        # every level down to odd extents
+        eng = hier.engine(ng, dt, r.device)
+        used = eng._tail()
+        assert (used is not None) == (tail == "1")
+        out[tail] = host(P.mg_correction(r, hier, n_sweeps=sweeps, finest_diag_scale=3.0).data)
+    if dt == F32:
+        assert np.array_equal(out["0"], out["1"])
+    else:
+        assert rel_l2(out["1"], out["0"]) < 1e-14
+
+
 def _cycle_setup(P, p, dt):
     from paper_2301_09991_b200 import benchmarks as B
     from paper_2301_09991_b200.problems import problem_from_data
