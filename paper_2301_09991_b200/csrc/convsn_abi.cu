@@ -475,24 +475,34 @@ int upwind_smooth_impl(const csn_geom* g, const void* src, int q_per_dof, int in
             // 1.99 -> 1.75 ms; with producer waits it had measured 1.18 vs 1.15 ms for
             // the register kernel)
             if (g_tune_upwind_tma && g1 && a.exact_div == 3 && init_mode != 1 && g->na >= 8 &&
-                g->na <= 32 && g->ny % 4 == 0 && !g->ghost_w && !g->ghost_e &&
+                g->na <= 32 && g->ny % 4 == 0 &&
                 (init_mode == 0 || (init_h == 0 && a.angle_coarsens))) {
                 UpTmaMaps maps;
+                // ghost x sides: the maps start H fine / 2 coarse columns before x = 0 and
+                // end as many past nx (the x-ghosted source, sigma and coarse correction of
+                // a DD rank); a physical side ends at the domain and TMA zero-fills
+                const int gw = g->ghost_w ? UP_H : 0, ge = g->ghost_e ? UP_H : 0;
+                const int cw = g->ghost_w ? (UP_H + 1) / 2 : 0, ce = g->ghost_e ? (UP_H + 1) / 2 : 0;
+                a.tma_xoff = gw;
+                a.tma_cxoff = cw;
                 const cuuint64_t C64 = (cuuint64_t)C;
-                cuuint64_t sd[3] = {C64, (cuuint64_t)g->ny, (cuuint64_t)g->nx};
+                cuuint64_t sd[3] = {C64, (cuuint64_t)g->ny, (cuuint64_t)(g->nx + gw + ge)};
                 cuuint64_t ss[2] = {C64 * 4, C64 * 4 * g->ny};
                 cuuint32_t sb[3] = {UPX_CC, UPT_ROWS, 1};
-                cuuint64_t gd[2] = {(cuuint64_t)g->ny, (cuuint64_t)g->nx};
+                cuuint64_t gd[2] = {(cuuint64_t)g->ny, (cuuint64_t)(g->nx + gw + ge)};
                 cuuint64_t gs[1] = {(cuuint64_t)g->ny * 4};
                 cuuint32_t gb[2] = {UPT_SIGROWS, 1};
-                bool ok = raw_map(&maps.src, src, 3, sd, ss, sb) &&
-                          raw_map(&maps.sigma, sigma, 2, gd, gs, gb);
+                bool ok = raw_map(&maps.src, (const float*)src - (int64_t)gw * g->ny * C, 3, sd,
+                                  ss, sb) &&
+                          raw_map(&maps.sigma, (const float*)sigma - (int64_t)gw * g->ny, 2, gd,
+                                  gs, gb);
                 if (ok && init_mode == 2) {
                     const cuuint64_t Cc = (cuuint64_t)gc->nd * gc->ng;
-                    cuuint64_t id[3] = {Cc, (cuuint64_t)gc->ny, (cuuint64_t)gc->nx};
+                    cuuint64_t id[3] = {Cc, (cuuint64_t)gc->ny, (cuuint64_t)(gc->nx + cw + ce)};
                     cuuint64_t is[2] = {Cc * 4, Cc * 4 * gc->ny};
                     cuuint32_t ib[3] = {UPT_CCH, UPT_CROWS, 1};
-                    ok = raw_map(&maps.init, init, 3, id, is, ib);
+                    ok = raw_map(&maps.init, (const float*)init - (int64_t)cw * gc->ny * Cc, 3,
+                                 id, is, ib);
                 } else if (ok) {
                     maps.init = maps.src;   // unused (mode 0)
                 }
