@@ -192,3 +192,31 @@ def test_z_fold_quadrature():
     np.testing.assert_array_equal(cf.directions, cq.directions[:cf.n_dir])
     with pytest.raises(ValueError):
         fold_z(f)
+
+
+def test_xwindow_views_and_ghost_flags():
+    """multigrid.XWindow (the launch geometry of an x-window of a slab, used to overlap the
+    DD halo exchange with the interior columns): narrowed views start at the window's first
+    column, a cut side is flagged ghost, an uncut side keeps the slab's flag."""
+    import torch
+    from paper_2301_09991_b200 import _lib
+    from paper_2301_09991_b200.multigrid import XWindow, _FullWindow
+    h, nx, ny, C = 3, 40, 6, 4
+    gm = _lib.geom(nx, ny, C, 1, 1, 0.5, 0.25, ghost_w=0, ghost_e=1)
+    padded = torch.arange((nx + 2 * h) * (ny + 2 * h) * C, dtype=torch.float32).reshape(
+        nx + 2 * h, ny + 2 * h, C)
+    cells = torch.arange(nx * ny, dtype=torch.float32).reshape(nx, ny)
+    w = XWindow(gm, 16, 24)
+    assert (w.gm.nx, w.gm.ny, w.gm.ghost_w, w.gm.ghost_e) == (8, ny, 1, 1)
+    assert (gm.nx, gm.ghost_w, gm.ghost_e) == (nx, 0, 1)          # the slab's geometry is untouched
+    v = w.pad(padded, h)
+    assert v.shape[0] == 8 + 2 * h and v.data_ptr() == padded[16].data_ptr()
+    assert torch.equal(v[h], padded[16 + h])                      # window column 0 = slab column 16
+    assert torch.equal(w.cells(cells), cells[16:24])
+    assert w.pad(None, h) is None and w.cells(None) is None
+    west = XWindow(gm, 0, 16, edge=True)
+    assert (west.gm.ghost_w, west.gm.ghost_e, west.edge) == (0, 1, True)   # physical west side kept
+    east = XWindow(gm, 24, nx, edge=True)
+    assert (east.gm.ghost_w, east.gm.ghost_e) == (1, 1)
+    full = _FullWindow(gm)
+    assert full.pad(padded, h) is padded and full.cells(cells) is cells and not full.edge
