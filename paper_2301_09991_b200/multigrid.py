@@ -116,8 +116,13 @@ def coarsen_sigma(sigma_t, eps=1e-30):
     """Harmonic 2x2 average; a zero child forces a zero parent (R/multigrid.py:70-77)."""
     nx, ny, ng = sigma_t.shape
     blk = np.asarray(sigma_t).reshape(nx // 2, 2, ny // 2, 2, ng)
+    # the sum keeps the reference's expression (NumPy's order of the 4 additions depends on
+    # the shape); the zero mask is order-free, so it is OR-ed from the four strided children
     coarse = 4.0 / (1.0 / np.maximum(blk, eps)).sum(axis=(1, 3))
-    coarse[(blk == 0.0).any(axis=(1, 3))] = 0.0
+    zero = ((blk[:, 0, :, 0] == 0.0) | (blk[:, 0, :, 1] == 0.0) | (blk[:, 1, :, 0] == 0.0)
+            | (blk[:, 1, :, 1] == 0.0))
+    if zero.any():
+        coarse[zero] = 0.0
     return coarse
 
 
