@@ -901,11 +901,13 @@ class CycleEngine:
             ema = plan["ema"]
 
             def run(i, win):
+                # windowed stages are timed as a whole (below): K2 and K3 of the windows
+                # interleave on two streams
                 if plan["k2"] is not None:
                     avg_in, avg_out, mode, theta = plan["k2"]
                     nv = _Nvtx("csn.k_refresh")
                     nv.__enter__()
-                    t = self._t0()
+                    t = None if multi else self._t0()
                     diffusivities_into(win.pad(psi_in, h), g, nd, ng, na, fs, cfg, c0["mu"],
                                        c0["nu"], win.pad(kx, h), win.pad(ky, h), h,
                                        avg_in=win.pad(avg_in, h), avg_out=win.pad(avg_out, h),
@@ -915,7 +917,7 @@ class CycleEngine:
                     nv.__exit__()
                 nv = _Nvtx("csn.residual")
                 nv.__enter__()
-                t = self._t0()
+                t = None if multi else self._t0()
                 v = Field.__new__(Field)
                 v.grid = g
                 v.data = win.pad(psi_in, h)
@@ -931,7 +933,10 @@ class CycleEngine:
                 self._t1("pg_residual" if ema[1] == 0 else "pg_residual+ema", t)
                 nv.__exit__()
 
+            t = self._t0() if multi else None
             self._run_windows(wins, exch, run)
+            self._t1(("pg_diffusivity+residual" if plan["k2"] is not None else "pg_residual+ema"
+                      if ema[1] else "pg_residual") + " (windowed)", t)
             if multi:              # fixed-order fp64 sum of the windows' L1
                 torch.sum(self.l1w[:len(wins)], dim=0, keepdim=True, out=self.l1)
         else:
