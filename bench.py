@@ -152,10 +152,10 @@ def workload(name, nx=None, world=1, n_a=None, slabs=None):
         # single-domain reference of a DD plumbing check); n_a: fewer ordinates (checks)
         return B.c5_weak(slabs or world, **({"n_a": n_a} if n_a else {}))
     if name == "c5":
-        if world < 4:
+        if world < 4 and not n_a:
             raise SystemExit("c5 (1024^2 x 2048 ordinates x 7 groups, 60.8 GB per fp32 "
                              "field) needs >= 4 GPUs; use c5w for the per-GPU weak variant")
-        return B.c5()
+        return B.c5(**({"n_a": n_a} if n_a else {}))     # n_a: plumbing checks only
     raise SystemExit(f"unknown config {name}")
 
 
@@ -664,7 +664,7 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--nx", type=int, default=None, help="override the cell count (c4 only)")
     ap.add_argument("--na", type=int, default=None,
-                    help="override n_a (c4, c5w; plumbing checks, not a BASELINE config)")
+                    help="override n_a (c4, c5, c5w; plumbing checks, not a BASELINE config)")
     ap.add_argument("--slabs", type=int, default=None,
                     help="c5w: the weak problem of this many ranks, (512 S) x 512, on any world")
     ap.add_argument("--dtype", default="float32")
