@@ -367,6 +367,7 @@ def make_krylov():
 PIN = {
     "c4_64n8": lambda: B.c4(nx=64, blocks=4, n_a=8, cycles=20),
     "c4_128n8": lambda: B.c4(nx=128, blocks=8, n_a=8, cycles=20),
+    "c4_256n8": lambda: B.c4(nx=256, blocks=16, n_a=8, cycles=20),
 }
 FLOOR = {
     "c1_alpha_r": lambda: B.c1(pg_off="alpha_r"),
