@@ -727,6 +727,7 @@ def test_integration_stub(P):
 PINNED = {
     "c4_64n8": lambda B: B.c4(nx=64, blocks=4, n_a=8, cycles=20),
     "c4_128n8": lambda B: B.c4(nx=128, blocks=8, n_a=8, cycles=20),
+    "c4_256n8": lambda B: B.c4(nx=256, blocks=16, n_a=8, cycles=20),
     "c4_reduced": DRIVERS["c4_reduced"][0],
     "c2_full": DRIVERS["c2_full"][0],
 }
