@@ -368,6 +368,10 @@ PIN = {
     "c4_64n8": lambda: B.c4(nx=64, blocks=4, n_a=8, cycles=20),
     "c4_128n8": lambda: B.c4(nx=128, blocks=8, n_a=8, cycles=20),
     "c4_256n8": lambda: B.c4(nx=256, blocks=16, n_a=8, cycles=20),
+    # the linear-PG multigroup kernels at the bench's channel widths (1024 and 3584
+    # channels: 2-group / generic-group TMA residual and sweep, fused K2, packed smoothers)
+    "c3_64n8": lambda: B.c3(n_pins=4, cells_per_pin=16, n_a=8, outers=6, inner=5),
+    "c5_64n8": lambda: B.c5(n_pins=4, cells_per_pin=16, n_a=8, outers=4, inner=3),
 }
 FLOOR = {
     "c1_alpha_r": lambda: B.c1(pg_off="alpha_r"),

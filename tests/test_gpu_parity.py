@@ -728,6 +728,10 @@ PINNED = {
     "c4_64n8": lambda B: B.c4(nx=64, blocks=4, n_a=8, cycles=20),
     "c4_128n8": lambda B: B.c4(nx=128, blocks=8, n_a=8, cycles=20),
     "c4_256n8": lambda B: B.c4(nx=256, blocks=16, n_a=8, cycles=20),
+    # linear PG, 2 and 7 groups at the bench's channel widths (1024 / 3584 channels): the
+    # 2-group and generic-group TMA residual / sweep, the fused K2, the packed smoothers
+    "c3_64n8": lambda B: B.c3(n_pins=4, cells_per_pin=16, n_a=8, outers=6, inner=5),
+    "c5_64n8": lambda B: B.c5(n_pins=4, cells_per_pin=16, n_a=8, outers=4, inner=3),
     "c4_reduced": DRIVERS["c4_reduced"][0],
     "c2_full": DRIVERS["c2_full"][0],
 }
@@ -751,6 +755,9 @@ def test_headline_kernels_pinned(P, tag, dtype):
     np.testing.assert_allclose(res.residual_history, g["residual_history"],
                                rtol=1e-9 if dtype == "float64" else 1e-4)
     np.testing.assert_array_equal(_log(res), g["pg_log"])
+    if "k_history" in g.files:           # north-star bar on k: 1e-6
+        np.testing.assert_allclose(res.history, g["k_history"],
+                                   rtol=1e-12 if dtype == "float64" else 1e-6)
     print(f"PIN {tag} {dtype} phi_rel_l2 {err:.3e} bound {tol:.3e}")
 
 
