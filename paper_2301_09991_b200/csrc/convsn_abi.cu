@@ -38,6 +38,7 @@ int g_tune_sweep_div = 1;
 int g_tune_pg_tma = 1;
 int g_tune_upwind_tma = 1;   // TMA-staged smoother columns (last releaser refills): C4 correction 1.99 -> 1.75 ms
 int g_tune_k2_tma = 1;   // TMA-staged K2b (last releaser refills its ring slot): C4 K2 4.04 -> 3.93 ms; the cp.async K2b was faster before that refill scheme (2.09 vs 2.18 ms)
+int g_tune_tail_smem = 1;   // coarse tail: levels <= 2048 DOF in CTA 0's shared memory
 int g_tune_k2_ws = 0;
 int g_tune_pg_xb = 0;   // x-blocked residual / sweep (warps per CTA: 4 or 8; 0 = off)   // one-pass K2: 5.0 ms vs 4.2 ms split on C4 (stage 2 starved)
 
@@ -122,7 +123,8 @@ inline int up_chunks0(int nx) { return (int)cdiv(nx, 8); }
 inline int up_chunks(int nx, int64_t ctas_xy, int min_cols) {
     int chunks = up_chunks0(nx);
     while (chunks > 1 && ctas_xy * (chunks / 2) >= 148 * 8) chunks /= 2;
-    while (cdiv(nx, chunks * 2) >= min_cols && ctas_xy * chunks * 2 <= 148 * 2) chunks *= 2;
+    while (chunks < nx && cdiv(nx, chunks * 2) >= min_cols && ctas_xy * chunks * 2 <= 148 * 2)
+        chunks *= 2;
     return chunks;
 }
 
@@ -582,6 +584,7 @@ int csn_set_tuning(const char* key, int value, int* prev) {
     if (!key) return CSN_E_ARG;
     int* slot = nullptr;
     if (!strcmp(key, "upwind_x2")) slot = &g_tune_upwind_x2;
+    if (!strcmp(key, "tail_smem")) slot = &g_tune_tail_smem;
     if (!strcmp(key, "upwind_div")) slot = &g_tune_upwind_div;
     if (!strcmp(key, "sweep_div")) slot = &g_tune_sweep_div;
     if (!strcmp(key, "pg_tma")) slot = &g_tune_pg_tma;
@@ -794,6 +797,9 @@ int csn_coarse_tail(int dtype, int n, const csn_geom* geoms, const void* const* 
         for (int i = 0; i < n; ++i) {
             TailLevel<Real>& L = t.lv[i];
             L.g = make_geo(geoms[i]);
+            L.dv.C = make_fastdiv(L.g.C); L.dv.ny = make_fastdiv(L.g.ny);
+            L.dv.ng = make_fastdiv(L.g.ng); L.dv.per = make_fastdiv(L.g.na * L.g.na);
+            L.dv.na = make_fastdiv(L.g.na);
             L.sigma = (const Real*)sigma[i];
             L.mu = (const Real*)mu[i]; L.nu = (const Real*)nu[i];
             L.strm = (const Real*)strm[i]; L.w = (const Real*)w[i];
@@ -804,9 +810,34 @@ int csn_coarse_tail(int dtype, int n, const csn_geom* geoms, const void* const* 
         t.scratch = (Real*)scratch;
         t.n_sweeps = n_sweeps;
         t.exact_div = std::is_same<Real, float>::value ? g_tune_upwind_div : 0;
+        // levels of <= TAIL_SMEM_DOF unknowns (never the tail's first: its source is the
+        // caller's) are solved in CTA 0's shared memory
+        t.n_smem_first = n;
+        for (int i = n - 1; i >= 1; --i) {
+            const int64_t dof = (int64_t)geoms[i].nx * geoms[i].ny * geoms[i].nd * geoms[i].ng;
+            if (dof > TAIL_SMEM_DOF || !g_tune_tail_smem) break;
+            t.n_smem_first = i;
+        }
+        int off = 0;
+        for (int i = 0; i < TAIL_MAX_LEVELS; ++i) {
+            t.smem_off[i] = 0;
+            if (i >= t.n_smem_first && i < n) {
+                t.smem_off[i] = off;
+                off += geoms[i].nx * geoms[i].ny * geoms[i].nd * geoms[i].ng;
+            }
+        }
+        if (off > TAIL_SMEM_SUM) return CSN_E_ARG;
+        constexpr size_t smem = coarse_tail_smem<Real>();
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(coarse_tail_kernel<Real>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(TAIL_CTAS);
         cfg.blockDim = dim3(TAIL_THREADS);
+        cfg.dynamicSmemBytes = smem;
         cfg.stream = S(stream);
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;

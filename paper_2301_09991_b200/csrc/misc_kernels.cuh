@@ -33,18 +33,28 @@ struct RestrictArgs {
 // done once per thread, the cell loop is loads + the reference's arithmetic order.  With angle coarsening and
 // ng == 1 the two column children (pb = 0, 1) are adjacent channels: one 8-byte load.
 // (restrict_cells: coarse channel cc over the coarse cells cell0, cell0 + stride, ...)
-template <class Real>
+// Quotients of the coarse level's index decomposition (by ng, n_a^2, n_a, ny): plain
+// division here; the coarse-tail kernel passes precomputed multipliers (FastDivs)
+struct PlainDivs {
+    int ng_, per_, na_, ny_;
+    __device__ __forceinline__ int by_ng(int v) const { return v / ng_; }
+    __device__ __forceinline__ int by_per(int v) const { return v / per_; }
+    __device__ __forceinline__ int by_na(int v) const { return v / na_; }
+    __device__ __forceinline__ int by_ny(int v) const { return v / ny_; }
+};
+
+template <class Real, class DV>
 __device__ __forceinline__ void restrict_cells(const RestrictArgs<Real>& a, const int cc,
-                                               const int cell0, const int stride) {
+                                               const int cell0, const int stride, const DV dv) {
     const Geo &gf = a.gf, &gc = a.gc;
-    const int N = cc / gc.ng, g = cc - N * gc.ng;
+    const int N = dv.by_ng(cc), g = cc - N * gc.ng;
     int cf[4];          // fine child channels (pa, pb) = (0,0), (0,1), (1,0), (1,1)
     Real wn[4];
     int nch = 1;
     if (a.angle_coarsens) {
         const int naf = gf.na, nac = gc.na;
-        const int f = N / (nac * nac), rem = N - f * nac * nac;
-        const int R = rem / nac, Cc = rem - R * nac;
+        const int f = dv.by_per(N), rem = N - f * nac * nac;
+        const int R = dv.by_na(rem), Cc = rem - R * nac;
 #pragma unroll
         for (int pa = 0; pa < 2; ++pa)
 #pragma unroll
@@ -64,7 +74,7 @@ __device__ __forceinline__ void restrict_cells(const RestrictArgs<Real>& a, cons
     const int64_t fpitch = (int64_t)(gf.ny + 2 * a.fine_h) * gf.C;   // x stride (fine)
     const int ncells = gc.nx * gc.ny;
     for (int cell = cell0; cell < ncells; cell += stride) {
-        const int I = cell / gc.ny, J = cell - I * gc.ny;
+        const int I = dv.by_ny(cell), J = cell - I * gc.ny;
         const Real* f0 = a.fine + fidx(2 * I, 2 * J, 0, gf.ny, a.fine_h, gf.C);
         Real acc = Real(0);
         if (pair) {
@@ -109,7 +119,8 @@ template <class Real>
 __global__ void __launch_bounds__(256) restrict_kernel(const RestrictArgs<Real> a) {
     const int cc = blockIdx.x * blockDim.x + threadIdx.x;
     if (cc >= a.gc.C) return;
-    restrict_cells(a, cc, (int)blockIdx.y, (int)gridDim.y);
+    restrict_cells(a, cc, (int)blockIdx.y, (int)gridDim.y,
+                   PlainDivs{a.gc.ng, a.gc.na * a.gc.na, a.gc.na, a.gc.ny});
 }
 
 template <class Real>

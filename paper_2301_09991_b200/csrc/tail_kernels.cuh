@@ -1,5 +1,5 @@
 // Coarse tail of the correction in ONE launch (R/multigrid.py:309-339 on the levels that
-// hold at most a few DOF per thread of one CTA): the restriction chain down from the
+// hold at most a few DOF per thread of one cluster): the restriction chain down from the
 // tail's finest level, then upwind Jacobi sweeps from the coarsest level up with the
 // piecewise-constant prolongation as each level's initial iterate.
 //
@@ -34,9 +34,32 @@ __device__ __forceinline__ void cluster_sync_all() {
                  "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+// Exact quotient by a precomputed multiplier: for 0 <= v and v * d < 2^32 (here v, d <=
+// 32768), floor(v / d) = umulhi(v, floor(2^32 / d) + 1).  An index decomposition by
+// hardware-emulated division was 60% of the tail kernel's instructions.
+struct FastDiv {
+    unsigned m;      // 0: divisor 1
+    __device__ __forceinline__ int operator()(int v) const {
+        return m ? (int)__umulhi((unsigned)v, m) : v;
+    }
+};
+inline FastDiv make_fastdiv(int d) {
+    FastDiv f;
+    f.m = d <= 1 ? 0u : (unsigned)((1ull << 32) / (unsigned)d) + 1u;
+    return f;
+}
+struct FastDivs {
+    FastDiv C, ny, ng, per, na;
+    __device__ __forceinline__ int by_ng(int v) const { return ng(v); }
+    __device__ __forceinline__ int by_per(int v) const { return per(v); }
+    __device__ __forceinline__ int by_na(int v) const { return na(v); }
+    __device__ __forceinline__ int by_ny(int v) const { return ny(v); }
+};
+
 template <class Real>
 struct TailLevel {
     Geo g;
+    FastDivs dv;         // by C, ny, ng, n_a^2, n_a of this level
     const Real* sigma;   // [nx][ny][ng]
     const Real* mu; const Real* nu; const Real* strm; const Real* w;   // [nd]
     Real* src;           // [nx][ny][C]: given on level 0 of the tail, restricted below
@@ -51,6 +74,8 @@ struct TailArgs {
     Real* scratch;                           // >= the largest tail level's DOF
     int n_sweeps;
     int exact_div;                           // fp32 update form (csn_set_tuning "upwind_div")
+    int n_smem_first;                        // first level held in CTA 0's shared memory (n: none)
+    int smem_off[TAIL_MAX_LEVELS];           // element offset of a shared level in s_src / s_del
 };
 
 // one update with the scalar smoother's form selection (upwind_smooth_kernel)
@@ -63,95 +88,182 @@ __device__ __forceinline__ Real tail_update(int form, Real ce, Real xu, Real yu,
     return up_update(ce, xu, yu, amx, amy, sg, sv, inv, d);
 }
 
+// loads of data produced inside the launch: L2 (ld.global.cg) for the levels shared by the
+// cluster's CTAs, plain (generic) loads for the levels CTA 0 keeps in shared memory
+template <bool CG, class Real>
+__device__ __forceinline__ Real tail_ld(const Real* p) { return CG ? __ldcg(p) : *p; }
+
+// parent channel of fine channel c on the next coarser level (R/multigrid.py:130-146)
+__device__ __forceinline__ int tail_parent(const Geo& g, const FastDivs& dv, const Geo& gc,
+                                           bool ac, int c) {
+    if (!ac) return c;
+    const int n = dv.ng(c), gg = c - n * g.ng;
+    const int per = g.na * g.na, f = dv.per(n), rem = n - f * per;
+    const int row = dv.na(rem), col = rem - row * g.na;
+    return (f * gc.na * gc.na + (row >> 1) * gc.na + (col >> 1)) * g.ng + gg;
+}
+
+// Element range [first, total) with stride `stride` of level L: restriction of the finer
+// source `fine` (level Lf) into `src`
+template <class Real>
+__device__ __forceinline__ void tail_restrict(const TailLevel<Real>& Lf, const TailLevel<Real>& Lc,
+                                              const Real* fine, Real* coarse, int first, int stride) {
+    RestrictArgs<Real> a;
+    a.gf = Lf.g; a.gc = Lc.g;
+    a.fine = fine; a.fine_h = 0;
+    a.wf = Lf.w; a.wc = Lc.w;
+    a.af = Lf.area; a.ac = Lc.area;
+    a.angle_coarsens = Lc.g.na != Lf.g.na;
+    a.normalise = 1;
+    a.coarse = coarse; a.coarse_h = 0;
+    const int C = Lc.g.C, total = C * Lc.g.nx * Lc.g.ny;
+    for (int e = first; e < total; e += stride) {
+        const int cell = Lc.dv.C(e);
+        restrict_cells(a, e - cell * C, cell, 1 << 30, Lc.dv);
+    }
+}
+
+// One Jacobi sweep of level L over the element range: sweep 0 starts from the prolongation
+// of the coarser correction cd (zero when there is none), later sweeps from `in`
+template <bool CG, class Real>
+__device__ __forceinline__ void tail_sweep(const TailLevel<Real>& L, const Geo& gc, bool has_c,
+                                           const Real* __restrict__ cd,
+                                           const Real* __restrict__ src,
+                                           const Real* __restrict__ in, Real* __restrict__ out,
+                                           bool first_sweep, int form, int first, int stride) {
+    const Geo& g = L.g;
+    const int C = g.C, ny = g.ny, nx = g.nx, total = C * nx * ny;
+    const bool ac = has_c && gc.na != g.na;
+    // the iterations are independent (in, out, src, cd never alias): unrolled so the loads
+    // of four elements are in flight together
+#pragma unroll 4
+    for (int e = first; e < total; e += stride) {
+        const int cell = L.dv.C(e), c = e - cell * C;
+        const int x = L.dv.ny(cell), y = cell - x * ny;
+        const int n = L.dv.ng(c), gg = c - n * g.ng;
+        const Real mu = L.mu[n], nu = L.nu[n];
+        const int xu_ = mu > Real(0) ? x - 1 : x + 1;
+        const int yu_ = nu > Real(0) ? y - 1 : y + 1;
+        const bool xin = xu_ >= 0 && xu_ < nx, yin = yu_ >= 0 && yu_ < ny;
+        Real ce, xu, yu;
+        if (first_sweep) {
+            if (!has_c) {
+                ce = xu = yu = Real(0);
+            } else {
+                const Real* cp = cd + tail_parent(g, L.dv, gc, ac, c);
+                ce = tail_ld<CG>(cp + ((int64_t)(x >> 1) * gc.ny + (y >> 1)) * gc.C);
+                xu = xin ? tail_ld<CG>(cp + ((int64_t)(xu_ >> 1) * gc.ny + (y >> 1)) * gc.C) : Real(0);
+                yu = yin ? tail_ld<CG>(cp + ((int64_t)(x >> 1) * gc.ny + (yu_ >> 1)) * gc.C) : Real(0);
+            }
+        } else {
+            ce = tail_ld<CG>(in + e);
+            xu = xin ? tail_ld<CG>(in + ((int64_t)xu_ * ny + y) * C + c) : Real(0);
+            yu = yin ? tail_ld<CG>(in + ((int64_t)x * ny + yu_) * C + c) : Real(0);
+        }
+        const Real amx = fabs(mu) * L.inv_dx, amy = fabs(nu) * L.inv_dy;
+        const Real sg = L.sigma[(int64_t)cell * g.ng + gg];
+        const Real d = Real(1) * (L.strm[n] + sg);
+        const Real inv = up_div(Real(1), d);
+        out[e] = tail_update(form, ce, xu, yu, amx, amy, sg, tail_ld<CG>(src + e), inv, d);
+    }
+}
+
+// n_sweeps == 0: the level's correction is the prolonged coarser one (or zero)
+template <bool CG, class Real>
+__device__ __forceinline__ void tail_inject(const TailLevel<Real>& L, const Geo& gc, bool has_c,
+                                            const Real* cd, Real* out, int first, int stride) {
+    const Geo& g = L.g;
+    const int C = g.C, ny = g.ny, total = C * g.nx * ny;
+    const bool ac = has_c && gc.na != g.na;
+    for (int e = first; e < total; e += stride) {
+        Real v = Real(0);
+        if (has_c) {
+            const int cell = L.dv.C(e), c = e - cell * C;
+            const int x = L.dv.ny(cell), y = cell - x * ny;
+            v = tail_ld<CG>(cd + ((int64_t)(x >> 1) * gc.ny + (y >> 1)) * gc.C +
+                            tail_parent(g, L.dv, gc, ac, c));
+        }
+        out[e] = v;
+    }
+}
+
+// Levels of <= TAIL_SMEM_DOF unknowns live in CTA 0's shared memory (their sources, their
+// corrections and one ping-pong buffer): a stage there is a loop and a __syncthreads()
+// with ~30-cycle loads instead of a cluster barrier and L2 round trips, which is what the
+// five or six smallest levels cost (20 stages of ~1.5 us -> ~3 us in all).
+constexpr int TAIL_SMEM_DOF = 2048;
+constexpr int TAIL_SMEM_SUM = 2048 + 1024;      // >= sum of the shared levels' DOF (each <= 1/2 the finer)
+
+template <class Real>
+constexpr size_t coarse_tail_smem() { return (size_t)(2 * TAIL_SMEM_SUM + TAIL_SMEM_DOF) * sizeof(Real); }
+
 template <class Real>
 __global__ void __launch_bounds__(TAIL_THREADS, 1) coarse_tail_kernel(const TailArgs<Real> t) {
+    extern __shared__ __align__(16) unsigned char tail_smraw[];
+    Real* s_src = reinterpret_cast<Real*>(tail_smraw);          // shared levels' sources
+    Real* s_del = s_src + TAIL_SMEM_SUM;                         // ... corrections
+    Real* s_tmp = s_del + TAIL_SMEM_SUM;                         // ... ping-pong buffer
     const int tid = blockIdx.x * TAIL_THREADS + threadIdx.x;     // grid = one cluster
-    // ---- restriction chain: src[i] from src[i - 1]
-    for (int i = 1; i < t.n; ++i) {
-        const TailLevel<Real>& lf = t.lv[i - 1];
-        const TailLevel<Real>& lc = t.lv[i];
-        RestrictArgs<Real> a;
-        a.gf = lf.g; a.gc = lc.g;
-        a.fine = lf.src; a.fine_h = 0;
-        a.wf = lf.w; a.wc = lc.w;
-        a.af = lf.area; a.ac = lc.area;
-        a.angle_coarsens = lc.g.na != lf.g.na;
-        a.normalise = 1;
-        a.coarse = lc.src; a.coarse_h = 0;
-        const int C = lc.g.C, total = C * lc.g.nx * lc.g.ny;
-        for (int e = tid; e < total; e += TAIL_STRIDE)
-            restrict_cells(a, e % C, e / C, 1 << 30);
+    // ns: first level kept in shared memory (t.n when none); levels [0, ns) are the cluster's
+    const int ns = t.n_smem_first;
+    // ---- restriction chain on the cluster's levels: src[i] from src[i - 1]
+    for (int i = 1; i < ns; ++i) {
+        tail_restrict(t.lv[i - 1], t.lv[i], t.lv[i - 1].src, t.lv[i].src, tid, TAIL_STRIDE);
         cluster_sync_all();
     }
-    // ---- smoothing, coarsest level up; sweep s reads `in` (the prolonged coarser
-    //      correction, or zero, for s = 0) and writes the buffer whose last turn is delta
-    for (int i = t.n - 1; i >= 0; --i) {
-        const TailLevel<Real>& L = t.lv[i];
-        const Geo& g = L.g;
-        const int C = g.C, ny = g.ny, nx = g.nx, total = C * nx * ny;
-        const bool has_c = i + 1 < t.n;
-        const Geo gc = has_c ? t.lv[i + 1].g : g;
-        const Real* cd = has_c ? t.lv[i + 1].delta : nullptr;
-        const bool ac = has_c && gc.na != g.na;
-        if (t.n_sweeps == 0) {
-            for (int e = tid; e < total; e += TAIL_STRIDE) {
-                Real v = Real(0);
-                if (has_c) {
-                    const int c = e % C, cell = e / C, y = cell % ny, x = cell / ny;
-                    int pc = c;
-                    if (ac) {
-                        const int n = c / g.ng, gg = c - n * g.ng;
-                        const int per = g.na * g.na, f = n / per, rem = n - f * per;
-                        const int row = rem / g.na, col = rem - row * g.na;
-                        pc = (f * gc.na * gc.na + (row >> 1) * gc.na + (col >> 1)) * g.ng + gg;
-                    }
-                    v = __ldcg(cd + ((int64_t)(x >> 1) * gc.ny + (y >> 1)) * gc.C + pc);
-                }
-                L.delta[e] = v;
+    // ---- the shared-memory levels, CTA 0 alone: restriction down, smoothing up
+    if (ns < t.n && blockIdx.x == 0) {
+        const int ltid = threadIdx.x;
+        int off = 0;
+        for (int i = ns; i < t.n; ++i) {
+            const Real* fine = i == ns ? t.lv[i - 1].src : s_src + t.smem_off[i - 1];
+            tail_restrict(t.lv[i - 1], t.lv[i], fine, s_src + off, ltid, TAIL_THREADS);
+            off += t.lv[i].g.C * t.lv[i].g.nx * t.lv[i].g.ny;
+            __syncthreads();
+        }
+        for (int i = t.n - 1; i >= ns; --i) {
+            const TailLevel<Real>& L = t.lv[i];
+            const bool has_c = i + 1 < t.n;
+            const Geo gc = has_c ? t.lv[i + 1].g : L.g;
+            const Real* cd = has_c ? s_del + t.smem_off[i + 1] : nullptr;
+            Real* del = s_del + t.smem_off[i];
+            const Real* src = s_src + t.smem_off[i];
+            if (t.n_sweeps == 0) {
+                tail_inject<false>(L, gc, has_c, cd, del, ltid, TAIL_THREADS);
+                __syncthreads();
             }
+            for (int s = 0; s < t.n_sweeps; ++s) {
+                const bool odd = (t.n_sweeps - 1 - s) & 1;
+                tail_sweep<false>(L, gc, has_c, cd, src, odd ? del : s_tmp, odd ? s_tmp : del,
+                                  s == 0, t.exact_div, ltid, TAIL_THREADS);
+                __syncthreads();
+            }
+            // the ABI's outputs: this level's source and correction, to global memory
+            const int total = L.g.C * L.g.nx * L.g.ny;
+            for (int e = ltid; e < total; e += TAIL_THREADS) {
+                L.src[e] = src[e];
+                L.delta[e] = del[e];
+            }
+        }
+    }
+    if (ns < t.n && ns > 0) cluster_sync_all();     // delta[ns] is visible to the cluster
+    // ---- smoothing of the cluster's levels, coarsest up; sweep s reads `in` (the prolonged
+    //      coarser correction, or zero, for s = 0) and writes the buffer whose last turn is delta
+    for (int i = ns - 1; i >= 0; --i) {
+        const TailLevel<Real>& L = t.lv[i];
+        const bool has_c = i + 1 < t.n;
+        const Geo gc = has_c ? t.lv[i + 1].g : L.g;
+        const Real* cd = has_c ? t.lv[i + 1].delta : nullptr;
+        if (t.n_sweeps == 0) {
+            tail_inject<true>(L, gc, has_c, cd, L.delta, tid, TAIL_STRIDE);
             cluster_sync_all();
             continue;
         }
         for (int s = 0; s < t.n_sweeps; ++s) {
             // the last sweep writes delta: buffers alternate backwards from it
-            Real* out = ((t.n_sweeps - 1 - s) & 1) ? t.scratch : L.delta;
-            const Real* in = ((t.n_sweeps - 1 - s) & 1) ? L.delta : t.scratch;
-            for (int e = tid; e < total; e += TAIL_STRIDE) {
-                const int c = e % C, cell = e / C, y = cell % ny, x = cell / ny;
-                const int n = c / g.ng, gg = c - n * g.ng;
-                const Real mu = L.mu[n], nu = L.nu[n];
-                const int xu_ = mu > Real(0) ? x - 1 : x + 1;
-                const int yu_ = nu > Real(0) ? y - 1 : y + 1;
-                const bool xin = xu_ >= 0 && xu_ < nx, yin = yu_ >= 0 && yu_ < ny;
-                Real ce, xu, yu;
-                if (s == 0) {
-                    if (!has_c) {
-                        ce = xu = yu = Real(0);
-                    } else {
-                        int pc = c;
-                        if (ac) {
-                            const int per = g.na * g.na, f = n / per, rem = n - f * per;
-                            const int row = rem / g.na, col = rem - row * g.na;
-                            pc = (f * gc.na * gc.na + (row >> 1) * gc.na + (col >> 1)) * g.ng + gg;
-                        }
-                        const Real* cp = cd + pc;
-                        ce = __ldcg(cp + ((int64_t)(x >> 1) * gc.ny + (y >> 1)) * gc.C);
-                        xu = xin ? __ldcg(cp + ((int64_t)(xu_ >> 1) * gc.ny + (y >> 1)) * gc.C)
-                                 : Real(0);
-                        yu = yin ? __ldcg(cp + ((int64_t)(x >> 1) * gc.ny + (yu_ >> 1)) * gc.C)
-                                 : Real(0);
-                    }
-                } else {
-                    ce = __ldcg(in + e);
-                    xu = xin ? __ldcg(in + ((int64_t)xu_ * ny + y) * C + c) : Real(0);
-                    yu = yin ? __ldcg(in + ((int64_t)x * ny + yu_) * C + c) : Real(0);
-                }
-                const Real amx = fabs(mu) * L.inv_dx, amy = fabs(nu) * L.inv_dy;
-                const Real sg = L.sigma[(int64_t)cell * g.ng + gg];
-                const Real d = Real(1) * (L.strm[n] + sg);
-                const Real inv = up_div(Real(1), d);
-                out[e] = tail_update(t.exact_div, ce, xu, yu, amx, amy, sg, __ldcg(L.src + e), inv, d);
-            }
+            const bool odd = (t.n_sweeps - 1 - s) & 1;
+            tail_sweep<true>(L, gc, has_c, cd, L.src, odd ? L.delta : t.scratch,
+                             odd ? t.scratch : L.delta, s == 0, t.exact_div, tid, TAIL_STRIDE);
             cluster_sync_all();
         }
     }
