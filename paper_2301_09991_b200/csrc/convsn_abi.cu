@@ -129,9 +129,13 @@ inline int up_chunks(int nx, int64_t ctas_xy, int min_cols) {
 }
 
 // rows per CTA chunk for the y-marching kernels: enough CTAs to fill 148 SMs ~4x
+// (a grid still below one wave of 2 CTAs/SM — a 64 x 64 x 128 problem is 16 tiles — is split
+// on down to one unroll group of rows per CTA: a CTA's march is a chain of dependent row
+// steps, and with most SMs idle the 2l lead-in rows of the extra chunks cost nothing)
 inline int pick_ly(int64_t ctas_xy, int rows, int T) {
     int chunks = 1;
     while (ctas_xy * chunks < 148 * 4 && rows / (chunks * 2) >= 4 * T) chunks *= 2;
+    while (ctas_xy * chunks * 2 <= 148 * 2 && rows / (chunks * 2) >= T) chunks *= 2;
     int ly = (int)cdiv(rows, chunks);
     ly = (int)cdiv(ly, T) * T;
     return ly;
