@@ -38,6 +38,7 @@ int g_tune_sweep_div = 1;
 int g_tune_pg_tma = 1;
 int g_tune_upwind_tma = 1;   // TMA-staged smoother columns (last releaser refills): C4 correction 1.99 -> 1.75 ms
 int g_tune_k2_tma = 1;   // TMA-staged K2b (last releaser refills its ring slot): C4 K2 4.04 -> 3.93 ms; the cp.async K2b was faster before that refill scheme (2.09 vs 2.18 ms)
+int g_tune_pg_chunks = 0;   // y chunks of the PG marches: 0 = cost model (pick_ly), n = forced
 int g_tune_tail_smem = 1;   // coarse tail: levels <= 2048 DOF in CTA 0's shared memory
 int g_tune_k2_ws = 0;
 int g_tune_pg_xb = 0;   // x-blocked residual / sweep (warps per CTA: 4 or 8; 0 = off)   // one-pass K2: 5.0 ms vs 4.2 ms split on C4 (stage 2 starved)
@@ -128,17 +129,38 @@ inline int up_chunks(int nx, int64_t ctas_xy, int min_cols) {
     return chunks;
 }
 
-// rows per CTA chunk for the y-marching kernels: enough CTAs to fill 148 SMs ~4x
-// (a grid still below one wave of 2 CTAs/SM — a 64 x 64 x 128 problem is 16 tiles — is split
-// on down to one unroll group of rows per CTA: a CTA's march is a chain of dependent row
-// steps, and with most SMs idle the 2l lead-in rows of the extra chunks cost nothing)
-inline int pick_ly(int64_t ctas_xy, int rows, int T) {
-    int chunks = 1;
-    while (ctas_xy * chunks < 148 * 4 && rows / (chunks * 2) >= 4 * T) chunks *= 2;
-    while (ctas_xy * chunks * 2 <= 148 * 2 && rows / (chunks * 2) >= T) chunks *= 2;
-    int ly = (int)cdiv(rows, chunks);
-    ly = (int)cdiv(ly, T) * T;
-    return ly;
+// Rows per CTA chunk of the y-marching kernels: a measured cost model (tools/ab_chunks.sh).
+// A CTA marches S = ly + 2l + 3 row steps (lead-in rows and start-up included) and the grid
+// runs in R = CTAs / resident slots rounds of equally long CTAs; a last round at most half
+// full runs ~1/0.65 faster (one CTA per SM).  Grids of fewer than 3 rounds made of 1 or 2
+// chunks measured 10% / 5% slower per row than 4+ chunks (every CTA walks the same rows in
+// lockstep), which the model carries as a factor.  The chunk count (a power of two, ly a
+// multiple of the march's unroll T) minimises rounds x S:
+//   * C4 residual / sweep: 2048 tiles = 6.9 rounds of 296 slots stay one chunk; its K2a
+//     (3.6 rounds of 592 slots) takes 4 chunks (C4 K2 3.93 -> 3.76 ms);
+//   * C3 fused K2: 304 tiles on 296 slots was 2 chunks = 2.05 rounds, now 4 = 4.1 rounds;
+//   * a 64-column DD slab (256 tiles) takes 4 chunks instead of 1; C1 (16 tiles) splits
+//     down to one unroll group per CTA.
+// slots: resident CTAs of the kernel on the whole GPU.
+inline int pick_ly(int64_t ctas_xy, int rows, int T, int L, int slots = 148 * 2) {
+    if (g_tune_pg_chunks > 0)       // A/B: forced chunk count
+        return (int)cdiv(cdiv(rows, g_tune_pg_chunks), T) * T;
+    int best_ly = (int)cdiv(rows, T) * T;
+    double best = 1e300;
+    for (int chunks = 1; chunks <= 64 && rows / chunks >= T; chunks *= 2) {
+        const int ly = (int)cdiv(cdiv(rows, chunks), T) * T;
+        const int64_t ctas = ctas_xy * cdiv(rows, ly);
+        const int64_t full = ctas / slots;
+        const double frac = (double)(ctas - full * slots) / slots;
+        double rounds = (double)full + (frac > 0.5 ? 1.0 : frac > 0.0 ? 0.65 : 0.0);
+        if ((double)ctas / slots < 3.0) rounds *= chunks == 1 ? 1.10 : chunks == 2 ? 1.05 : 1.0;
+        const double cost = rounds * (ly + 2 * L + 3);
+        if (cost < best * 0.999) {      // ties keep the fewer, longer chunks
+            best = cost;
+            best_ly = ly;
+        }
+    }
+    return best_ly;
 }
 
 // The kernels use the compile-time unit taps of taps_table.cuh; the caller's taps
@@ -202,7 +224,7 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
     const int gx = (int)cdiv(g->nx, PG_TX);
     const int gy = (int)cdiv((int64_t)g->nd * g->ng, X2 ? X2_CC : PG_CC);
     // y chunks a multiple of the TMA march's unroll (2T at L = 1, see TmaRing)
-    a.ly = pick_ly((int64_t)gx * gy, g->ny, X2 && L == 1 ? 2 * T : T);
+    a.ly = pick_ly((int64_t)gx * gy, g->ny, X2 && L == 1 ? 2 * T : T, L);
     const int gz = (int)cdiv(g->ny, a.ly);
     a.partials = (l1 || partials) ? partials : nullptr;
     dim3 grid(gx, gy, gz), block(PG_CC, PG_TX);
@@ -214,7 +236,7 @@ int pg_residual_impl(const csn_geom* g, const double* taps, const void* psi, int
             if ((g_tune_pg_xb == 4 || g_tune_pg_xb == 8) && vec && dterm_mode == 0) {
                 const int nw = g_tune_pg_xb;
                 const int gxb = (int)cdiv(g->nx, 2 * nw);
-                a.ly = pick_ly((int64_t)gxb * gy, g->ny, T);
+                a.ly = pick_ly((int64_t)gxb * gy, g->ny, T, L);
                 const int gzb = (int)cdiv(g->ny, a.ly);
                 dim3 gridb(gxb, gy, gzb), blockb(32, nw);
                 if (!out && l1 && !partials) return CSN_E_ARG;
@@ -348,7 +370,7 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
       if (work && g_tune_k2_ws) {   // one pass, warp-specialised (no workspace traffic)
         const int gx = (int)cdiv(g->nx + 2 * L, WS_TX);
         const int gy = (int)cdiv((int64_t)g->nd * g->ng, X2_CC);
-        a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T);
+        a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T, 2 * L, 148);
         dim3 grid(gx, gy, (int)cdiv(g->ny + 2 * L, a.ly)), block(32, 2 * WS_TX + 2 * L);
         if (avg_mode == 2) {
             if (vec) launch_pg_k_ws<L, true, V>(grid, block, st, a);
@@ -368,7 +390,7 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
         dim3 block(32, PG_TX);
         {
             const int gx = (int)cdiv(g->nx + 4 * L, PG_TX);
-            a.ly = pick_ly((int64_t)gx * gy, g->ny + 4 * L, T);
+            a.ly = pick_ly((int64_t)gx * gy, g->ny + 4 * L, T, L, 148 * (L >= 3 ? 4 : 3));
             dim3 grid(gx, gy, (int)cdiv(g->ny + 4 * L, a.ly));
             if (avg_mode == 2) {
                 if (vec) launch_pg_grad_x2<L, true, V>(grid, block, st, a, gxp, gyp, gh);
@@ -381,7 +403,7 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
         }
         {
             const int gx = (int)cdiv(g->nx + 2 * L, PG_TX);
-            a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T);
+            a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T, L, 148 * 3);
             dim3 grid(gx, gy, (int)cdiv(g->ny + 2 * L, a.ly));
             // TMA staging of the workspace rows (k2_tma), else the cp.async stager
             KcoefMaps km;     // the workspace is a field with halo gh = 2l
@@ -401,7 +423,7 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
         constexpr int TXO2 = X2_KT - 2 * L;
         const int gx = (int)cdiv(g->nx + 2 * L, TXO2);
         const int gy = (int)cdiv((int64_t)g->nd * g->ng, X2_CC);
-        a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T);
+        a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T, 2 * L, L == 1 ? 148 * 2 : 148);
         const int gz = (int)cdiv(g->ny + 2 * L, a.ly);
         dim3 grid(gx, gy, gz), block(32, X2_KT);
         if (avg_mode == 2) {
@@ -417,7 +439,7 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
     } else {
     const int gx = (int)cdiv(g->nx + 2 * L, TXO);
     const int gy = (int)cdiv((int64_t)g->nd * g->ng, PG_CC);
-    a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T);
+    a.ly = pick_ly((int64_t)gx * gy, g->ny + 2 * L, T, 2 * L, 148);
     const int gz = (int)cdiv(g->ny + 2 * L, a.ly);
     dim3 grid(gx, gy, gz), block(PG_CC, KT);
     if (avg_mode == 2) {
@@ -589,6 +611,7 @@ int csn_set_tuning(const char* key, int value, int* prev) {
     int* slot = nullptr;
     if (!strcmp(key, "upwind_x2")) slot = &g_tune_upwind_x2;
     if (!strcmp(key, "tail_smem")) slot = &g_tune_tail_smem;
+    if (!strcmp(key, "pg_chunks")) slot = &g_tune_pg_chunks;
     if (!strcmp(key, "upwind_div")) slot = &g_tune_upwind_div;
     if (!strcmp(key, "sweep_div")) slot = &g_tune_sweep_div;
     if (!strcmp(key, "pg_tma")) slot = &g_tune_pg_tma;
