@@ -362,6 +362,11 @@ int pg_k_impl(const csn_geom* g, const double* taps, const double* cfg, const vo
     a.eps = (Real)cfg[0]; a.alpha_r = (Real)cfg[1]; a.a_abs = (Real)cfg[2]; a.a_sq = (Real)cfg[3];
     a.dx = (Real)g->dx; a.dy = (Real)g->dy;
     a.inv_dx = (Real)(1.0 / g->dx); a.inv_dy = (Real)(1.0 / g->dy);
+    {   // single rounded products in Real, as the device multiplication gave
+        volatile Real cax = a.a_abs * a.dx, csx = a.a_sq * a.dx, cay = a.a_abs * a.dy,
+                      csy = a.a_sq * a.dy;
+        a.cax = cax; a.csx = csx; a.cay = cay; a.csy = csy;
+    }
     a.mu = (const Real*)mu; a.nu = (const Real*)nu;
     a.kx = (Real*)kx; a.ky = (Real*)ky; a.k_h = k_h;
     constexpr int V = 16 / sizeof(Real);

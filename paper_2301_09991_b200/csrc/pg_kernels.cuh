@@ -297,6 +297,9 @@ struct PGKArgs {
     Real* avg_out; int avg_out_h;
     int avg_mode; Real theta, omt;
     Real alpha_r, eps, a_abs, a_sq, dx, dy, inv_dx, inv_dy;
+    // a_abs dx, a_sq dx, a_abs dy, a_sq dy formed once on the host (the same rounded
+    // products the kernels used to recompute for every k: ptxas did not keep them live)
+    Real cax, csx, cay, csy;
     const Real* mu; const Real* nu;
     Real* kx; Real* ky; int k_h;
     int ly;     // output rows per CTA chunk (band coordinates), multiple of T

@@ -435,9 +435,9 @@ pg_kcoef_tma_kernel(const PGKArgs<float> a, const __grid_constant__ KcoefMaps m,
             const float rxv[2] = {rx.x, rx.y}, ryv[2] = {ry.x, ry.y};                     \
             float kx[2], ky[2];                                                           \
             _Pragma("unroll") for (int h = 0; h < 2; ++h) {                               \
-                kx[h] = k_coef(rxv[h], pxv[h], a.a_abs * a.dx, a.a_sq * a.dx,             \
+                kx[h] = k_coef(rxv[h], pxv[h], a.cax, a.csx,             \
                                a.dx * amu[h], amu[h], a.eps);                             \
-                ky[h] = k_coef(ryv[h], pyv[h], a.a_abs * a.dy, a.a_sq * a.dy,             \
+                ky[h] = k_coef(ryv[h], pyv[h], a.cay, a.csy,             \
                                a.dy * anu[h], anu[h], a.eps);                             \
             }                                                                             \
             const int64_t o = kb0 + (int64_t)(Y) * g.C;                                   \
@@ -690,9 +690,9 @@ pg_k_ws_kernel(const PGKArgs<float> a) {
                 const float rxv[2] = {rx.x, rx.y}, ryv[2] = {ry.x, ry.y};                 \
                 float kx[2], ky[2];                                                       \
                 _Pragma("unroll") for (int h = 0; h < 2; ++h) {                           \
-                    kx[h] = k_coef(rxv[h], pxv[h], a.a_abs * a.dx, a.a_sq * a.dx,         \
+                    kx[h] = k_coef(rxv[h], pxv[h], a.cax, a.csx,         \
                                    a.dx * amu[h], amu[h], a.eps);                         \
-                    ky[h] = k_coef(ryv[h], pyv[h], a.a_abs * a.dy, a.a_sq * a.dy,         \
+                    ky[h] = k_coef(ryv[h], pyv[h], a.cay, a.csy,         \
                                    a.dy * anu[h], anu[h], a.eps);                         \
                 }                                                                         \
                 const int64_t o = kb0 + (int64_t)(Y) * g.C;                               \

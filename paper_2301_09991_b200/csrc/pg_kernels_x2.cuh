@@ -461,9 +461,9 @@ pg_diffusivity_x2_kernel(const PGKArgs<float> a) {
                     float kx[2], ky[2];
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        kx[h] = k_coef(rxv[h], pxv[h], a.a_abs * a.dx, a.a_sq * a.dx,
+                        kx[h] = k_coef(rxv[h], pxv[h], a.cax, a.csx,
                                        a.dx * amu[h], amu[h], a.eps);
-                        ky[h] = k_coef(ryv[h], pyv[h], a.a_abs * a.dy, a.a_sq * a.dy,
+                        ky[h] = k_coef(ryv[h], pyv[h], a.cay, a.csy,
                                        a.dy * anu[h], anu[h], a.eps);
                     }
                     const int64_t o = kbase_o + (int64_t)(vo - L) * g.C;
@@ -707,9 +707,9 @@ pg_kcoef_x2_kernel(const PGKArgs<float> a, const float* __restrict__ gx_in,
         const float rxv[2] = {rx.x, rx.y}, ryv[2] = {ry.x, ry.y};                                  \
         float kx[2], ky[2];                                                                        \
         _Pragma("unroll") for (int h = 0; h < 2; ++h) {                                                    \
-            kx[h] = k_coef(rxv[h], pxv[h], a.a_abs * a.dx, a.a_sq * a.dx, a.dx * amu[h],         \
+            kx[h] = k_coef(rxv[h], pxv[h], a.cax, a.csx, a.dx * amu[h],         \
                            amu[h], a.eps);                                                       \
-            ky[h] = k_coef(ryv[h], pyv[h], a.a_abs * a.dy, a.a_sq * a.dy, a.dy * anu[h],         \
+            ky[h] = k_coef(ryv[h], pyv[h], a.cay, a.csy, a.dy * anu[h],         \
                            anu[h], a.eps);                                                       \
         }                                                                                        \
         const int64_t o = kb0 + (int64_t)(Y) * g.C;                                                \
