@@ -335,9 +335,17 @@ struct KcoefMaps {
     CUtensorMap gx, gy;
 };
 
+// ring depth of the TMA K2b: L + 1 rows held for the output's centre + CSN_K2B_PREFETCH in
+// flight ahead of the lead row
+#ifndef CSN_K2B_PREFETCH
+#define CSN_K2B_PREFETCH (L <= 3 ? X2_PREFETCH : 2)
+#endif
+template <int L>
+struct K2bStages { static constexpr int value = L + 1 + CSN_K2B_PREFETCH; };
+
 template <int L>
 constexpr size_t pg_kcoef_tma_smem() {
-    return (size_t)X2Stages<L>::value * 2 * (PG_TX + 2 * L) * X2_CC * sizeof(float) + 128;
+    return (size_t)K2bStages<L>::value * 2 * (PG_TX + 2 * L) * X2_CC * sizeof(float) + 128;
 }
 
 // 3 CTAs/SM (78 registers); 4 (64 registers, 36 B of spills) measured C4 K2 3.92 -> 4.07 ms
@@ -351,7 +359,7 @@ pg_kcoef_tma_kernel(const PGKArgs<float> a, const __grid_constant__ KcoefMaps m,
     constexpr int T = 2 * L + 1;
     constexpr int CC = X2_CC;
     constexpr int W = PG_TX + 2 * L;
-    constexpr int S = X2Stages<L>::value;
+    constexpr int S = K2bStages<L>::value;
     constexpr int P = S - L - 1;
     constexpr int FS = W * CC;
     constexpr int SLOT = 2 * FS;
@@ -404,6 +412,14 @@ pg_kcoef_tma_kernel(const PGKArgs<float> a, const __grid_constant__ KcoefMaps m,
     float2 r2x[T], r2y[T];   // M_x psi_x, M_x psi_y by lead row (step mod T)
     int slot = 0;
     unsigned fpar = 0;
+    // per-lane constants of the k formula, kept live (opaque to the optimiser, which
+    // otherwise recomputes the six products at every output: 3% of the kernel's issue)
+    float2 armu = make_float2(a.alpha_r * mu0, a.alpha_r * mu1);
+    float2 arnu = make_float2(a.alpha_r * nu0, a.alpha_r * nu1);
+    float capx0 = a.dx * fabsf(mu0), capx1 = a.dx * fabsf(mu1);
+    float capy0 = a.dy * fabsf(nu0), capy1 = a.dy * fabsf(nu1);
+    asm volatile("" : "+f"(armu.x), "+f"(armu.y), "+f"(arnu.x), "+f"(arnu.y), "+f"(capx0),
+                      "+f"(capx1), "+f"(capy0), "+f"(capy1));
 
 #define K2BT_STEP(K, KR, OUT, Y)                                                         \
     {                                                                                     \
@@ -426,19 +442,16 @@ pg_kcoef_tma_kernel(const PGKArgs<float> a, const __grid_constant__ KcoefMaps m,
             }                                                                             \
             const float* cb = sm + cs_ * SLOT + L * CC + lane;                            \
             const float2 pxc = ld2(cb), pyc = ld2(cb + FS);                               \
-            const float2 rx = mul2(make_float2(a.alpha_r * mu0, a.alpha_r * mu1),         \
-                                   sub2(mmx, pxc));                                       \
-            const float2 ry = mul2(make_float2(a.alpha_r * nu0, a.alpha_r * nu1),         \
-                                   sub2(mmy, pyc));                                       \
+            const float2 rx = mul2(armu, sub2(mmx, pxc));                                 \
+            const float2 ry = mul2(arnu, sub2(mmy, pyc));                                 \
             const float amu[2] = {fabsf(mu0), fabsf(mu1)}, anu[2] = {fabsf(nu0), fabsf(nu1)}; \
+            const float capx[2] = {capx0, capx1}, capy[2] = {capy0, capy1};               \
             const float pxv[2] = {pxc.x, pxc.y}, pyv[2] = {pyc.x, pyc.y};                 \
             const float rxv[2] = {rx.x, rx.y}, ryv[2] = {ry.x, ry.y};                     \
             float kx[2], ky[2];                                                           \
             _Pragma("unroll") for (int h = 0; h < 2; ++h) {                               \
-                kx[h] = k_coef(rxv[h], pxv[h], a.cax, a.csx,             \
-                               a.dx * amu[h], amu[h], a.eps);                             \
-                ky[h] = k_coef(ryv[h], pyv[h], a.cay, a.csy,             \
-                               a.dy * anu[h], anu[h], a.eps);                             \
+                kx[h] = k_coef(rxv[h], pxv[h], a.cax, a.csx, capx[h], amu[h], a.eps);     \
+                ky[h] = k_coef(ryv[h], pyv[h], a.cay, a.csy, capy[h], anu[h], a.eps);     \
             }                                                                             \
             const int64_t o = kb0 + (int64_t)(Y) * g.C;                                   \
             st2(a.kx + o, make_float2(kx[0], kx[1]));                                     \
