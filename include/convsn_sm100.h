@@ -78,6 +78,11 @@ const char* csn_error_string(int code);
  *                  bit-identical; measured slower on C4);
  *   "upwind_tma" = 0 (default): 1 stages the packed smoother's columns with TMA where
  *                  the layout allows (bit-identical; measured 3% slower on C4).
+ *   "tail_smem"  = 1 (default): csn_coarse_tail solves the levels of <= 2048 unknowns in one
+ *                  CTA's shared memory; 0 keeps every level on the cluster (bit-identical);
+ *   "pg_chunks"  = 0 (default): the y-chunk count of the PG marches comes from the cost
+ *                  model; n > 0 forces n chunks (A/B timing; fields are bit-identical, the
+ *                  fp64 L1 is summed in chunk order).
  * The previous value is stored in *prev (nullable). */
 int csn_set_tuning(const char* key, int value, int* prev);
 
