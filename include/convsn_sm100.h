@@ -71,13 +71,15 @@ const char* csn_error_string(int code);
  *                  0: reciprocal product;
  *   "pg_tma"     = 1 (default): fp32 csn_pg_residual stages padded fields with TMA
  *                  (mbarrier ring); 0 forces the cp.async kernel (bit-identical);
- *   "k2_tma"     = 0 (default): 1 stages the fp32 diffusivity path's second pass (k
- *                  from the workspace) with TMA (bit-identical; measured 4% slower);
+ *   "k2_tma"     = 1 (default): the fp32 diffusivity path's second pass (k from the
+ *                  workspace) stages its rows with TMA except at order 2 (2: always; 0: the
+ *                  cp.async stager; bit-identical);
  *   "k2_ws"      = 0 (default): 1 runs the workspace-path diffusivities as one
  *                  warp-specialised pass (psi_x, psi_y through shared memory;
  *                  bit-identical; measured slower on C4);
- *   "upwind_tma" = 0 (default): 1 stages the packed smoother's columns with TMA where
- *                  the layout allows (bit-identical; measured 3% slower on C4).
+ *   "upwind_tma" = 1 (default): the packed smoother stages its columns with TMA where the
+ *                  layout allows (one group, 8 <= n_a <= 32; ghost x sides included); 0: the
+ *                  register kernel (bit-identical);
  *   "tail_smem"  = 1 (default): csn_coarse_tail solves the levels of <= 2048 unknowns in one
  *                  CTA's shared memory; 0 keeps every level on the cluster (bit-identical);
  *   "pg_chunks"  = 0 (default): the y-chunk count of the PG marches comes from the cost
