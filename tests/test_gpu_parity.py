@@ -784,3 +784,36 @@ def test_folded_correction_bitwise(P, tag, dtype):
     np.testing.assert_array_equal(out[0].phi, out[1].phi)
     np.testing.assert_array_equal(out[0].residual_history, out[1].residual_history)
     assert out[0].pg_log == out[1].pg_log
+
+
+@pytest.mark.parametrize("nx,ny,na,p", [(24, 40, 2, 1), (40, 24, 4, 3), (64, 64, 8, 2), (16, 100, 2, 5),
+                                        (72, 136, 8, 3)])
+def test_pg_chunking_bitwise(P, nx, ny, na, p):
+    """The y-chunk count of the PG marches (pick_ly's cost model, csn_set_tuning pg_chunks)
+    changes only which CTA computes a row: psi after PG cycles is bit-identical for the
+    model's choice and for 1, 3 and 8 forced chunks, on ragged grids too; the fp64
+    residual L1 differs only by its summation order."""
+    from paper_2301_09991_b200 import _lib
+    from paper_2301_09991_b200 import benchmarks as B
+    from paper_2301_09991_b200.eigen import Solver
+    from paper_2301_09991_b200.problems import problem_from_data
+    pd = B.c2(nx=8, blocks=2, n_a=na, cycles=3)
+    rng = np.random.default_rng(nx * ny)
+    pd.nx, pd.ny = nx, ny
+    pd.region_map = rng.integers(0, len(pd.materials), size=(nx, ny))
+    pd.source = rng.uniform(0.0, 1.0, size=(nx, ny, 1))
+    pd.options["order"] = p
+    opts = P.SolverOptions(scheme="pg", order=p, n_a=na, mg_iters=3, bootstrap_cycles=0,
+                           n_levels=1 if (nx % 2 or ny % 2) else None, dtype="float32")
+    out = {}
+    for chunks in (0, 1, 3, 8):
+        prev = _lib.set_tuning("pg_chunks", chunks)
+        try:
+            s = Solver(problem_from_data(pd), opts, None)
+            res = s.run()
+            out[chunks] = (s.psi.data.clone(), np.array(res.residual_history))
+        finally:
+            _lib.set_tuning("pg_chunks", prev)
+    for chunks in (1, 3, 8):
+        assert torch.equal(out[chunks][0], out[0][0]), f"psi differs at pg_chunks={chunks}"
+        np.testing.assert_allclose(out[chunks][1], out[0][1], rtol=1e-12)
