@@ -817,3 +817,18 @@ def test_pg_chunking_bitwise(P, nx, ny, na, p):
     for chunks in (1, 3, 8):
         assert torch.equal(out[chunks][0], out[0][0]), f"psi differs at pg_chunks={chunks}"
         np.testing.assert_allclose(out[chunks][1], out[0][1], rtol=1e-12)
+
+
+def test_jacobi_diagonal_goldens(P):
+    """Public jacobi_diagonal (R/discretisation.py:97-111; the kernels form d per DOF on the
+    fly, this is the materialised API) against the reference's arrays for both schemes, and
+    its ValueError on an unknown scheme."""
+    g = golden("ops")
+    q = P.build_quadrature(2)
+    grid = P.GridSpec(9, 7, 0.3, 0.2, 1)
+    for scheme, key in (("upwind", "diag_up"), ("pg", "diag_pg")):
+        d = P.jacobi_diagonal(g["sigma"], q, grid, scheme)
+        assert d.is_cuda and d.dtype == torch.float64
+        np.testing.assert_allclose(host(d), g[key], rtol=1e-15)
+    with pytest.raises(ValueError):
+        P.jacobi_diagonal(g["sigma"], q, grid, "central")
