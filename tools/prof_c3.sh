@@ -8,6 +8,5 @@ cap() {
 }
 cap k5 "pg_residual_tma_kernel<.int.1, .int.3" 0
 cap k3 "pg_residual_tma_kernel<.int.1, .int.0" 0
-cap k2a "pg_grad_x2" 0
-cap k2b "pg_kcoef" 0
+cap k2 "pg_diffusivity_x2" 0
 cap up "upwind_smooth_x2" 1
