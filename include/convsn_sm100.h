@@ -80,6 +80,9 @@ const char* csn_error_string(int code);
  *   "upwind_tma" = 1 (default): the packed smoother stages its columns with TMA where the
  *                  layout allows (one group, 8 <= n_a <= 32; ghost x sides included); 0: the
  *                  register kernel (bit-identical);
+ *   "tail_faces" = 1 (default): csn_coarse_tail runs one CTA per (octahedron face, group),
+ *                  each level's slice in shared memory (no inter-CTA synchronisation); 0: the
+ *                  8-CTA cluster kernel (bit-identical);
  *   "tail_smem"  = 1 (default): csn_coarse_tail solves the levels of <= 2048 unknowns in one
  *                  CTA's shared memory; 0 keeps every level on the cluster (bit-identical);
  *   "pg_chunks"  = 0 (default): the y-chunk count of the PG marches comes from the cost

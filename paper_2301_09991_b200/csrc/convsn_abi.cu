@@ -39,6 +39,7 @@ int g_tune_pg_tma = 1;
 int g_tune_upwind_tma = 1;   // TMA-staged smoother columns (last releaser refills): C4 correction 1.99 -> 1.75 ms
 int g_tune_k2_tma = 1;   // TMA-staged K2b (last releaser refills its ring slot): C4 K2 4.04 -> 3.93 ms; the cp.async K2b was faster before that refill scheme (2.09 vs 2.18 ms)
 int g_tune_pg_chunks = 0;   // y chunks of the PG marches: 0 = cost model (pick_ly), n = forced
+int g_tune_tail_faces = 1;  // coarse tail: one CTA per (face, group) in shared memory; 0 = cluster kernel
 int g_tune_tail_smem = 1;   // coarse tail: levels <= 2048 DOF in CTA 0's shared memory
 int g_tune_k2_ws = 0;
 int g_tune_pg_xb = 0;   // x-blocked residual / sweep (warps per CTA: 4 or 8; 0 = off)   // one-pass K2: 5.0 ms vs 4.2 ms split on C4 (stage 2 starved)
@@ -616,6 +617,7 @@ int csn_set_tuning(const char* key, int value, int* prev) {
     int* slot = nullptr;
     if (!strcmp(key, "upwind_x2")) slot = &g_tune_upwind_x2;
     if (!strcmp(key, "tail_smem")) slot = &g_tune_tail_smem;
+    if (!strcmp(key, "tail_faces")) slot = &g_tune_tail_faces;
     if (!strcmp(key, "pg_chunks")) slot = &g_tune_pg_chunks;
     if (!strcmp(key, "upwind_div")) slot = &g_tune_upwind_div;
     if (!strcmp(key, "sweep_div")) slot = &g_tune_sweep_div;
@@ -838,10 +840,42 @@ int csn_coarse_tail(int dtype, int n, const csn_geom* geoms, const void* const* 
             L.src = (Real*)src[i]; L.delta = (Real*)delta[i];
             L.inv_dx = (Real)(1.0 / geoms[i].dx); L.inv_dy = (Real)(1.0 / geoms[i].dy);
             L.area = (Real)(geoms[i].dx * geoms[i].dy);
+            L.sig_stride = L.g.ng;
+            const int per = L.g.na * L.g.na;
+            L.fdv.C = make_fastdiv(per); L.fdv.ny = make_fastdiv(L.g.ny);
+            L.fdv.ng = make_fastdiv(1); L.fdv.per = make_fastdiv(per);
+            L.fdv.na = make_fastdiv(L.g.na);
+            L.face_off = 0;
         }
         t.scratch = (Real*)scratch;
         t.n_sweeps = n_sweeps;
         t.exact_div = std::is_same<Real, float>::value ? g_tune_upwind_div : 0;
+        // one CTA per (face, group), everything in shared memory, when every level's slice
+        // fits (csn_set_tuning "tail_faces", default on); else the cluster kernel
+        {
+            bool faces = g_tune_tail_faces != 0;
+            int off = 0;
+            for (int i = 0; i < n && faces; ++i) {
+                const int per = geoms[i].na * geoms[i].na;
+                const int64_t dof = (int64_t)geoms[i].nx * geoms[i].ny * per;
+                if (geoms[i].nd % per || dof > TAIL_FACE_DOF) faces = false;
+                t.lv[i].face_off = off;
+                off += (int)((dof + 1) & ~(int64_t)1);        // even: 8-byte pair loads
+            }
+            if (faces && off <= TAIL_FACE_SUM) {
+                constexpr size_t fsm = coarse_tail_face_smem<Real>();
+                static bool fattr = false;
+                if (!fattr) {
+                    cudaFuncSetAttribute(coarse_tail_face_kernel<Real>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+                    fattr = true;
+                }
+                const int nfaces = geoms[0].nd / (geoms[0].na * geoms[0].na);
+                coarse_tail_face_kernel<Real><<<nfaces * geoms[0].ng, TAIL_THREADS, fsm, S(stream)>>>(t);
+                CSN_CHECK_LAUNCH();
+                return CSN_OK;
+            }
+        }
         // levels of <= TAIL_SMEM_DOF unknowns (never the tail's first: its source is the
         // caller's) are solved in CTA 0's shared memory
         t.n_smem_first = n;

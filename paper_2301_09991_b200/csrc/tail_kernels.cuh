@@ -65,6 +65,9 @@ struct TailLevel {
     Real* src;           // [nx][ny][C]: given on level 0 of the tail, restricted below
     Real* delta;         // [nx][ny][C]: the level's smoothed correction (output)
     Real inv_dx, inv_dy, area;
+    int sig_stride;      // sigma of a cell: sigma[cell * sig_stride + group] (= ng)
+    FastDivs fdv;        // face-local decomposition: by n_a^2 (as C), ny, 1, n_a^2, n_a
+    int face_off;        // element offset of this level in the face kernel's shared arrays
 };
 
 template <class Real>
@@ -161,7 +164,7 @@ __device__ __forceinline__ void tail_sweep(const TailLevel<Real>& L, const Geo& 
             yu = yin ? tail_ld<CG>(in + ((int64_t)x * ny + yu_) * C + c) : Real(0);
         }
         const Real amx = fabs(mu) * L.inv_dx, amy = fabs(nu) * L.inv_dy;
-        const Real sg = L.sigma[(int64_t)cell * g.ng + gg];
+        const Real sg = L.sigma[(int64_t)cell * L.sig_stride + gg];
         const Real d = Real(1) * (L.strm[n] + sg);
         const Real inv = up_div(Real(1), d);
         out[e] = tail_update(form, ce, xu, yu, amx, amy, sg, tail_ld<CG>(src + e), inv, d);
@@ -265,6 +268,102 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) coarse_tail_kernel(const Tail
             tail_sweep<true>(L, gc, has_c, cd, L.src, odd ? L.delta : t.scratch,
                              odd ? t.scratch : L.delta, s == 0, t.exact_div, tid, TAIL_STRIDE);
             cluster_sync_all();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// The same tail, one CTA per (octahedron face, group), no inter-CTA synchronisation.
+// Every operator of the correction keeps a face's directions and a group to themselves:
+// the smoother couples only spatial neighbours of one channel, restriction sums the 2 x 2
+// patch children of one face (R/multigrid.py:342-353), prolongation injects a parent into
+// its children (R/multigrid.py:130-146).  So the tail splits into n_faces x n_group
+// independent problems of <= TAIL_FACE_DOF unknowns per level, each solved by one CTA
+// entirely in shared memory (a stage = a loop + __syncthreads()): the level-0 source
+// slice is gathered from global memory once, the results scattered back at the end.
+// Local layout of a level: [cell][patch r of the face] (a field with nd = n_a^2, ng = 1),
+// which restrict_cells / tail_sweep take as is with the face's slice of w, mu, nu, strm
+// and the group's sigma — the same rounded operations, bit-identical results.
+// Launch 55 us (level by level) -> 35 us (cluster) -> ~15 us.
+// ---------------------------------------------------------------------------------
+constexpr int TAIL_FACE_DOF = 4096;                      // per CTA and level (32768 per 8 faces)
+constexpr int TAIL_FACE_SUM = TAIL_FACE_DOF + TAIL_FACE_DOF / 4 + TAIL_FACE_DOF / 8;
+
+template <class Real>
+constexpr size_t coarse_tail_face_smem() {
+    return (size_t)(2 * TAIL_FACE_SUM + TAIL_FACE_DOF) * sizeof(Real);
+}
+
+template <class Real>
+__global__ void __launch_bounds__(TAIL_THREADS, 1) coarse_tail_face_kernel(const TailArgs<Real> t) {
+    extern __shared__ __align__(16) unsigned char tail_smraw[];
+    Real* s_src = reinterpret_cast<Real*>(tail_smraw);
+    Real* s_del = s_src + TAIL_FACE_SUM;
+    Real* s_tmp = s_del + TAIL_FACE_SUM;
+    const int ng = t.lv[0].g.ng;
+    const int face = blockIdx.x / ng, gq = blockIdx.x - face * ng;
+    const int tid = threadIdx.x;
+
+    // face-local view of level i: geometry of one face and one group, sliced pointers
+    auto view = [&](int i) {
+        TailLevel<Real> V = t.lv[i];
+        const int per = V.g.na * V.g.na;
+        V.g.nd = per; V.g.ng = 1; V.g.C = per;
+        V.dv = V.fdv;
+        V.mu += face * per; V.nu += face * per; V.strm += face * per; V.w += face * per;
+        V.sigma += gq;
+        return V;
+    };
+    // global element of local (cell, r) on level i
+    auto gidx = [&](const TailLevel<Real>& G, int cell, int r) {
+        const int per = G.g.na * G.g.na;
+        return (int64_t)cell * G.g.C + (face * per + r) * ng + gq;
+    };
+
+    {   // the CTA's slice of the given source
+        const TailLevel<Real>& G = t.lv[0];
+        const int per = G.g.na * G.g.na, total = G.g.nx * G.g.ny * per;
+        for (int e = tid; e < total; e += TAIL_THREADS) {
+            const int cell = G.fdv.C(e);
+            s_src[e] = G.src[gidx(G, cell, e - cell * per)];
+        }
+        __syncthreads();
+    }
+    for (int i = 1; i < t.n; ++i) {          // restriction chain
+        const TailLevel<Real> Vf = view(i - 1), Vc = view(i);
+        tail_restrict(Vf, Vc, s_src + Vf.face_off, s_src + Vc.face_off, tid, TAIL_THREADS);
+        __syncthreads();
+    }
+    for (int i = t.n - 1; i >= 0; --i) {     // smoothing, coarsest level up
+        const TailLevel<Real> V = view(i);
+        const bool has_c = i + 1 < t.n;
+        Geo gc = V.g;
+        if (has_c) {
+            gc = t.lv[i + 1].g;
+            gc.nd = gc.na * gc.na; gc.ng = 1; gc.C = gc.nd;
+        }
+        const Real* cd = has_c ? s_del + t.lv[i + 1].face_off : nullptr;
+        Real* del = s_del + V.face_off;
+        const Real* src = s_src + V.face_off;
+        if (t.n_sweeps == 0) {
+            tail_inject<false>(V, gc, has_c, cd, del, tid, TAIL_THREADS);
+            __syncthreads();
+        }
+        for (int s = 0; s < t.n_sweeps; ++s) {
+            const bool odd = (t.n_sweeps - 1 - s) & 1;
+            tail_sweep<false>(V, gc, has_c, cd, src, odd ? del : s_tmp, odd ? s_tmp : del, s == 0,
+                              t.exact_div, tid, TAIL_THREADS);
+            __syncthreads();
+        }
+    }
+    for (int i = 0; i < t.n; ++i) {          // the ABI's outputs, back in the global layout
+        const TailLevel<Real>& G = t.lv[i];
+        const int per = G.g.na * G.g.na, total = G.g.nx * G.g.ny * per;
+        for (int e = tid; e < total; e += TAIL_THREADS) {
+            const int cell = G.fdv.C(e);
+            const int64_t ge = gidx(G, cell, e - cell * per);
+            if (i > 0) G.src[ge] = s_src[G.face_off + e];
+            G.delta[ge] = s_del[G.face_off + e];
         }
     }
 }

@@ -167,18 +167,29 @@ def test_coarse_tail_matches_levels(P, na, ng, nx, ny, sweeps, dt, monkeypatch):
     rng = np.random.default_rng(nx * 131 + ng)
     sigma = rng.uniform(0.1, 8.0, size=(nx, ny, ng))
     r = torch.as_tensor(rng.standard_normal((nx, ny, q.n_dir, ng)), dtype=dt, device="cuda")
+    from paper_2301_09991_b200 import _lib
     out = {}
-    for tail in ("0", "1"):
-        monkeypatch.setenv("CSN_TAIL", tail)
-        hier = P.build_hierarchy(grid, q, sigma)        # every level down to odd extents
-        eng = hier.engine(ng, dt, r.device)
-        used = eng._tail()
-        assert (used is not None) == (tail == "1")
-        out[tail] = host(P.mg_correction(r, hier, n_sweeps=sweeps, finest_diag_scale=3.0).data)
-    if dt == F32:
-        assert np.array_equal(out["0"], out["1"])
-    else:
-        assert rel_l2(out["1"], out["0"]) < 1e-14
+    # "0": level by level; "faces": one CTA per (face, group) in shared memory (default);
+    # "cluster": the 8-CTA cluster kernel (with and without its shared-memory levels)
+    for tail, tune in (("0", {}), ("faces", {}), ("cluster", {"tail_faces": 0}),
+                       ("cluster_g", {"tail_faces": 0, "tail_smem": 0})):
+        monkeypatch.setenv("CSN_TAIL", "0" if tail == "0" else "1")
+        prev = {k: _lib.set_tuning(k, v) for k, v in tune.items()}
+        try:
+            hier = P.build_hierarchy(grid, q, sigma)        # every level down to odd extents
+            eng = hier.engine(ng, dt, r.device)
+            used = eng._tail()
+            assert (used is not None) == (tail != "0")
+            out[tail] = host(P.mg_correction(r, hier, n_sweeps=sweeps,
+                                             finest_diag_scale=3.0).data)
+        finally:
+            for k, v in prev.items():
+                _lib.set_tuning(k, v)
+    for tail in ("faces", "cluster", "cluster_g"):
+        if dt == F32:
+            assert np.array_equal(out["0"], out[tail]), tail
+        else:
+            assert rel_l2(out[tail], out["0"]) < 1e-14, tail
 
 
 def _cycle_setup(P, p, dt):
