@@ -846,6 +846,7 @@ int csn_coarse_tail(int dtype, int n, const csn_geom* geoms, const void* const* 
             L.fdv.ng = make_fastdiv(1); L.fdv.per = make_fastdiv(per);
             L.fdv.na = make_fastdiv(L.g.na);
             L.face_off = 0;
+            L.const_off = 0;
         }
         t.scratch = (Real*)scratch;
         t.n_sweeps = n_sweeps;
@@ -854,15 +855,17 @@ int csn_coarse_tail(int dtype, int n, const csn_geom* geoms, const void* const* 
         // fits (csn_set_tuning "tail_faces", default on); else the cluster kernel
         {
             bool faces = g_tune_tail_faces != 0;
-            int off = 0;
+            int off = 0, coff = 0;
             for (int i = 0; i < n && faces; ++i) {
                 const int per = geoms[i].na * geoms[i].na;
                 const int64_t dof = (int64_t)geoms[i].nx * geoms[i].ny * per;
                 if (geoms[i].nd % per || dof > TAIL_FACE_DOF) faces = false;
                 t.lv[i].face_off = off;
                 off += (int)((dof + 1) & ~(int64_t)1);        // even: 8-byte pair loads
+                t.lv[i].const_off = coff;
+                coff += 4 * per + geoms[i].nx * geoms[i].ny;
             }
-            if (faces && off <= TAIL_FACE_SUM) {
+            if (faces && off <= TAIL_FACE_SUM && coff <= TAIL_FACE_CONST) {
                 constexpr size_t fsm = coarse_tail_face_smem<Real>();
                 static bool fattr = false;
                 if (!fattr) {

@@ -68,6 +68,7 @@ struct TailLevel {
     int sig_stride;      // sigma of a cell: sigma[cell * sig_stride + group] (= ng)
     FastDivs fdv;        // face-local decomposition: by n_a^2 (as C), ny, 1, n_a^2, n_a
     int face_off;        // element offset of this level in the face kernel's shared arrays
+    int const_off;       // ... of its [mu | nu | strm | w | sigma] block in the constants area
 };
 
 template <class Real>
@@ -289,9 +290,11 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) coarse_tail_kernel(const Tail
 constexpr int TAIL_FACE_DOF = 4096;                      // per CTA and level (32768 per 8 faces)
 constexpr int TAIL_FACE_SUM = TAIL_FACE_DOF + TAIL_FACE_DOF / 4 + TAIL_FACE_DOF / 8;
 
+constexpr int TAIL_FACE_CONST = 2048;                    // per-level mu, nu, strm, w, sigma slices
+
 template <class Real>
 constexpr size_t coarse_tail_face_smem() {
-    return (size_t)(2 * TAIL_FACE_SUM + TAIL_FACE_DOF) * sizeof(Real);
+    return (size_t)(2 * TAIL_FACE_SUM + TAIL_FACE_DOF + TAIL_FACE_CONST) * sizeof(Real);
 }
 
 template <class Real>
@@ -300,18 +303,39 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) coarse_tail_face_kernel(const
     Real* s_src = reinterpret_cast<Real*>(tail_smraw);
     Real* s_del = s_src + TAIL_FACE_SUM;
     Real* s_tmp = s_del + TAIL_FACE_SUM;
+    Real* s_c = s_tmp + TAIL_FACE_DOF;       // every level's constants, loaded once up front
     const int ng = t.lv[0].g.ng;
     const int face = blockIdx.x / ng, gq = blockIdx.x - face * ng;
     const int tid = threadIdx.x;
 
-    // face-local view of level i: geometry of one face and one group, sliced pointers
+    // the face's mu, nu, strm, w and the group's sigma of every level into shared memory,
+    // in flight together with the source gather below (a stage otherwise starts with an
+    // L2 round trip for its level's constants)
+    {
+        const TailLevel<Real>& Gl = t.lv[t.n - 1];
+        const int total_c = Gl.const_off + 4 * Gl.g.na * Gl.g.na + Gl.g.nx * Gl.g.ny;
+        for (int ee = tid; ee < total_c; ee += TAIL_THREADS) {   // one flat loop: <= 2 per thread
+            int i = 0;
+            while (i + 1 < t.n && t.lv[i + 1].const_off <= ee) ++i;
+            const TailLevel<Real>& G = t.lv[i];
+            const int per = G.g.na * G.g.na, e = ee - G.const_off;
+            const int k = e < 4 * per ? G.fdv.C(e) : 4, r = e - k * per;
+            s_c[ee] = k == 0 ? G.mu[face * per + r] : k == 1 ? G.nu[face * per + r]
+                    : k == 2 ? G.strm[face * per + r] : k == 3 ? G.w[face * per + r]
+                             : G.sigma[(int64_t)r * ng + gq];
+        }
+    }
+
+    // face-local view of level i: geometry of one face and one group, constants in smem
     auto view = [&](int i) {
         TailLevel<Real> V = t.lv[i];
         const int per = V.g.na * V.g.na;
         V.g.nd = per; V.g.ng = 1; V.g.C = per;
         V.dv = V.fdv;
-        V.mu += face * per; V.nu += face * per; V.strm += face * per; V.w += face * per;
-        V.sigma += gq;
+        const Real* c = s_c + V.const_off;
+        V.mu = c; V.nu = c + per; V.strm = c + 2 * per; V.w = c + 3 * per;
+        V.sigma = c + 4 * per;
+        V.sig_stride = 1;
         return V;
     };
     // global element of local (cell, r) on level i
