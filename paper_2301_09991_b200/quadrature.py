@@ -11,6 +11,8 @@ patches at once (vectorised over the patch axis) and uploaded once per level.
 
 from dataclasses import dataclass
 
+import functools
+
 import numpy as np
 
 FOUR_PI = 4.0 * np.pi
@@ -109,10 +111,17 @@ def _patch_area_moment(p):
 
 
 def build_quadrature(n_a):
-    """``8 n_a^2`` ordinates with weights rescaled to sum to 4 pi (R/quadrature.py:112-151)."""
+    """``8 n_a^2`` ordinates with weights rescaled to sum to 4 pi (R/quadrature.py:112-151).
+
+    The set depends on n_a alone and its arrays are read-only, so it is built once per
+    n_a (and with it its coarsened chain and the device copies cached on the objects)."""
     if not isinstance(n_a, (int, np.integer)) or n_a < 1 or (n_a & (n_a - 1)) != 0:
         raise ValueError(f"n_a must be a positive power of 2, got {n_a!r}")
-    n_a = int(n_a)
+    return _build_quadrature(int(n_a))
+
+
+@functools.lru_cache(maxsize=16)
+def _build_quadrature(n_a):
     k = np.arange(n_a, dtype=float)
     t0, t1 = k / n_a, (k + 1) / n_a          # rows towards the pole
     s0, s1 = k / n_a, (k + 1) / n_a          # columns along the equator edge
@@ -142,14 +151,19 @@ def coarsen_quadrature(quad):
     """Merge 2x2 patch blocks per face: weights add, directions weight-average."""
     if quad.n_a < 2:
         raise ValueError("cannot coarsen: already at one patch per face")
+    memo = quad.__dict__.get("_coarse")          # the arrays are read-only: coarsen once
+    if memo is not None:
+        return memo
     m = quad.n_a // 2
     nf = quad.n_faces
     w = quad.weights.reshape(nf, m, 2, m, 2)
     d = quad.directions.reshape(nf, m, 2, m, 2, 3)
     wc = w.sum(axis=(2, 4))
     dc = (d * w[..., None]).sum(axis=(2, 4)) / wc[..., None]
-    return AngularQuadrature(n_a=m, directions=dc.reshape(-1, 3), weights=wc.reshape(-1),
-                             face_index=np.repeat(np.arange(nf), m * m), n_faces_=nf)
+    out = AngularQuadrature(n_a=m, directions=dc.reshape(-1, 3), weights=wc.reshape(-1),
+                            face_index=np.repeat(np.arange(nf), m * m), n_faces_=nf)
+    quad.__dict__["_coarse"] = out
+    return out
 
 
 def fold_z(quad):
