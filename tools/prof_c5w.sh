@@ -12,10 +12,11 @@ cap() {
   python tools/sass_hist.py gpurun_out/c5p_$1.ncu-rep "." 0 > gpurun_out/c5p_$1_hist.txt 2>&1
   [ "$KEEP" = "$1" ] || [ "$KEEP" = "all" ] || rm -f gpurun_out/c5p_$1.ncu-rep
 }
-for k in ${KERNELS:-k5 k3 k2a k2b up}; do
+for k in ${KERNELS:-k5 k3 k2 up}; do
   case $k in
     k5) cap k5 "pg_residual_tma_kernel<.int.1, .int.3" 0 ;;
     k3) cap k3 "pg_residual_tma_kernel<.int.1, .int.0" 0 ;;
+    k2) cap k2 "pg_diffusivity_x2" 0 ;;
     k2a) cap k2a "pg_grad_x2" 0 ;;
     k2b) cap k2b "pg_kcoef" 0 ;;
     up) cap up "upwind_smooth" 0 ;;
